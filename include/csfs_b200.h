@@ -1,0 +1,114 @@
+/*
+ * csfs_b200 — C-ABI of the B200-native (sm_100a) cubed-sphere FMM.
+ *
+ * Drop-in boundary for the reference library's summation engine
+ * (/root/reference/proj/include/csfs/summation.hpp).  Plain pointers and sizes only;
+ * positions are AoS x,y,z doubles exactly as std::vector<csfs::Vec3>::data() lays them
+ * out, weights/outputs are in INPUT order like the reference's ParticleSet /
+ * PotentialField (summation.hpp:34-41).  The C++ shim (paper_2508_13550_b200/csrc/host/
+ * csfs_b200.hpp) re-exposes the reference's csfs:: signatures on top of these entry
+ * points and rethrows std::invalid_argument on code 1 with the reference's messages.
+ *
+ * Return codes: 0 ok, 1 invalid argument (reference's std::invalid_argument),
+ * 2 CUDA error, 3 NCCL/collective error, 4 device out of memory.
+ * One context per host thread; a context owns one device, one stream and its buffers;
+ * calls on one context are serialized by the caller.
+ */
+#ifndef CSFS_B200_H
+#define CSFS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSFS_B200_OK 0
+#define CSFS_B200_INVALID_ARGUMENT 1
+#define CSFS_B200_CUDA_ERROR 2
+#define CSFS_B200_NCCL_ERROR 3
+#define CSFS_B200_OUT_OF_MEMORY 4
+
+typedef struct csfs_b200_ctx csfs_b200_ctx;
+
+/* csfs::Kernel (kernels.hpp:32-49): kind in KernelKind order
+ * 0 laplace, 1 biharmonic, 2 biot_savart (out_dim 3), 3 sal; SalParams defaults
+ * a1=-2.7, b0=-6.21196, b1=6.1, rho_ratio=1025/5517 (kernels.hpp:18-23). */
+typedef struct {
+    int kind;
+    double a1, b0, b1, rho_ratio;
+} csfs_b200_kernel;
+
+/* csfs::TraversalConfig (summation.hpp:22-31) minus method/threads:
+ * n0 < 0 selects 4*degree^2 (resolved_n0). */
+typedef struct {
+    double mac;
+    int degree;
+    int n0;
+    int shrink;
+} csfs_b200_config;
+
+/* csfs::SumStats (summation.hpp:44-53) plus B200 extras. Times in seconds, measured
+ * with CUDA events on the context stream. t_traversal = lists + PP/PC/CP/CC, as in the
+ * reference's csfmm_sum (summation.cpp:397-402). */
+typedef struct {
+    double t_tree_build, t_upward, t_traversal, t_downward, t_total;
+    uint64_t pp, pc, cp, cc;
+    int src_depth, src_clusters, src_leaves;
+    int tgt_depth, tgt_clusters, tgt_leaves;
+    double t_lists, t_interact;                  /* sub-phases of t_traversal */
+    uint64_t evals_pp, evals_pc, evals_cp, evals_cc; /* pairwise kernel evaluations */
+    int shared_tree;                             /* targets == sources: one tree built */
+} csfs_b200_stats;
+
+/* --- lifetime ------------------------------------------------------------------------ */
+int csfs_b200_create(csfs_b200_ctx** out, int device);
+void csfs_b200_destroy(csfs_b200_ctx* ctx);
+/* Message of the last failing call on this context ("" if none). */
+const char* csfs_b200_last_error(const csfs_b200_ctx* ctx);
+
+/* --- the hot path ---------------------------------------------------------------------
+ * csfs::csfmm_sum (summation.hpp:81-83, summation.cpp:383-421).  HOST pointers:
+ * tgt_xyz nt x 3, src_xyz ns x 3, src_w ns, out nt x out_dim (overwritten).
+ * stats may be NULL.  Synchronous. */
+int csfs_b200_csfmm(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt, const double* src_xyz,
+                    const double* src_w, size_t ns, const csfs_b200_kernel* kernel,
+                    const csfs_b200_config* config, double* out, csfs_b200_stats* stats);
+
+/* Same, DEVICE pointers (on the context's device), work ordered on `stream`
+ * (cudaStream_t, NULL = the context's own stream).  Returns after the result is in
+ * `out` (the engine synchronizes on tree/list sizes). */
+int csfs_b200_csfmm_device(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt,
+                           const double* src_xyz, const double* src_w, size_t ns,
+                           const csfs_b200_kernel* kernel, const csfs_b200_config* config,
+                           double* out, csfs_b200_stats* stats, void* stream);
+
+/* csfs::direct_sum (summation.hpp:74-75, summation.cpp:136-161): O(nt*ns) all pairs. */
+int csfs_b200_direct(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt, const double* src_xyz,
+                     const double* src_w, size_t ns, const csfs_b200_kernel* kernel, double* out);
+int csfs_b200_direct_device(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt,
+                            const double* src_xyz, const double* src_w, size_t ns,
+                            const csfs_b200_kernel* kernel, double* out, void* stream);
+
+/* --- stepwise state of the LAST csfmm call (parity / inspection) ------------------------
+ * which: 0 target tree, 1 source tree.  Cluster ids are the REFERENCE's ids
+ * (LIFO expansion order, cluster_tree.cpp:87-140). */
+int csfs_b200_tree_info(const csfs_b200_ctx* ctx, int which, int* n_clusters, int* depth,
+                        size_t* n_particles, int* n_proxy_per_cluster);
+/* perm: n (tree order -> input index); ints: ncl x 10 = face, begin, end, parent, depth,
+ * child_count, children[4]; dbls: ncl x 8 = xi0, xi1, eta0, eta1, cx, cy, cz, radius;
+ * proxy: ncl x (p+1)^2 x 3.  Any pointer may be NULL. */
+int csfs_b200_tree_export(csfs_b200_ctx* ctx, int which, int* perm, int* ints, double* dbls,
+                          double* proxy);
+/* counts[4] = |pp|,|pc|,|cp|,|cc|; lists as (t, s) int pairs in reference ids, sorted. */
+int csfs_b200_lists_export(csfs_b200_ctx* ctx, long long* counts, int* pp, int* pc, int* cp,
+                           int* cc);
+/* Source-tree proxy weights after the upward pass, ncl x (p+1)^2, reference id order. */
+int csfs_b200_proxy_weights_export(csfs_b200_ctx* ctx, double* pw);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSFS_B200_H */

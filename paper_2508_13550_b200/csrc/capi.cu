@@ -1,0 +1,438 @@
+// C-ABI of the B200 CSFMM (include/csfs_b200.h) and the orchestration that replaces
+// csfs::csfmm_sum (/root/reference/proj/src/summation.cpp:383-421):
+//   tree build (targets, sources) -> upward pass -> dual traversal -> PP/PC/CP/CC
+//   -> downward pass, every phase a device kernel on the context's stream, phase times
+//   from CUDA events (the reference's steady_clock SumStats, summation.cpp:407-419).
+// There is no CPU fallback: without a usable sm_100a device every call fails.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/csfs_b200.h"
+#include "engine.hpp"
+
+using namespace csfs_b200;
+
+struct csfs_b200_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    std::string err;
+    DeviceTree ttree, stree;
+    bool shared = false;
+    Scratch sc;
+    Lists lists;
+    Items items;
+    DevBuf<double> phi_near;
+    DevBuf<int> counter;
+    DevBuf<double> h_txyz, h_sxyz, h_w, h_out;  // staging for the host-pointer API
+    DevBuf<double> d_soa;
+    DevBuf<int4> d_items;
+    DevBuf<int2> d_segs;
+    cudaEvent_t ev[8] = {};
+    Cheb cheb{};
+    KernelSpec kspec;
+    FmmConfig cfg;
+    bool have_state = false;
+    int dim = 1;
+    int n_internal_t = 0, n_internal_s = 0;
+};
+
+namespace {
+
+int fail(csfs_b200_ctx* c, int code, const std::string& m) {
+    if (c) c->err = m;
+    return code;
+}
+
+template <class F>
+int guarded(csfs_b200_ctx* c, F&& f) {
+    if (!c) return CSFS_B200_INVALID_ARGUMENT;
+    try {
+        CSFS_CK(cudaSetDevice(c->device));
+        f();
+        c->err.clear();
+        return CSFS_B200_OK;
+    } catch (const InvalidArgument& e) {
+        return fail(c, CSFS_B200_INVALID_ARGUMENT, e.what());
+    } catch (const OutOfMemory& e) {
+        return fail(c, CSFS_B200_OUT_OF_MEMORY, e.what());
+    } catch (const CudaFailure& e) {
+        return fail(c, CSFS_B200_CUDA_ERROR, e.what());
+    } catch (const std::exception& e) {
+        return fail(c, CSFS_B200_CUDA_ERROR, e.what());
+    }
+}
+
+KernelSpec to_spec(const csfs_b200_kernel* k) {
+    if (!k) throw InvalidArgument("kernel must not be null");
+    if (k->kind < 0 || k->kind > 3) throw InvalidArgument("unknown kernel kind: " + std::to_string(k->kind));
+    KernelSpec s;
+    s.kind = k->kind;
+    s.a1 = k->a1;
+    s.b0 = k->b0;
+    s.b1 = k->b1;
+    s.rho_ratio = k->rho_ratio;
+    return s;
+}
+
+FmmConfig to_cfg(const csfs_b200_config* c) {
+    if (!c) throw InvalidArgument("config must not be null");
+    FmmConfig f;
+    f.mac = c->mac;
+    f.degree = c->degree;
+    f.n0 = c->n0;
+    f.shrink = c->shrink != 0;
+    return f;
+}
+
+// Validation in the reference's order: ChebyshevGrid1D (interpolation.cpp:15), then the
+// ClusterTree checks (cluster_tree.cpp:32-33), targets first.
+void validate(const FmmConfig& f, size_t nt, size_t ns) {
+    if (f.degree < 1) throw InvalidArgument("interpolation degree must be positive");
+    if (f.degree > kMaxNp - 1)
+        throw InvalidArgument("interpolation degree above " + std::to_string(kMaxNp - 1) +
+                              " is not supported by the B200 engine");
+    if (nt == 0 || ns == 0) throw InvalidArgument("cannot build a cluster tree from an empty particle set");
+    if (f.resolved_n0() < 1) throw InvalidArgument("maximum leaf size must be at least 1");
+    if (nt > 0x3fffffff || ns > 0x3fffffff) throw InvalidArgument("particle count exceeds 2^30");
+}
+
+Cheb make_cheb(int degree) {
+    // ChebyshevGrid1D (interpolation.cpp:14-24), same libm call on the host.
+    Cheb c{};
+    c.np = degree + 1;
+    for (int k = 0; k <= degree; ++k) {
+        c.nodes[k] = std::cos(k * kPi / degree);
+        c.weights[k] = (k % 2 == 0) ? 1.0 : -1.0;
+    }
+    c.weights[0] *= 0.5;
+    c.weights[degree] *= 0.5;
+    return c;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    CSFS_CK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+int count_internal(const DeviceTree& t) {
+    std::vector<int> nch(t.ncl);
+    CSFS_CK(cudaMemcpy(nch.data(), t.nchild.p, t.ncl * sizeof(int), cudaMemcpyDeviceToHost));
+    int k = 0;
+    for (int v : nch) k += v > 0;
+    return k;
+}
+
+void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
+               const double* sw, size_t ns, const KernelSpec& ks, const FmmConfig& f, double* out,
+               csfs_b200_stats* st, cudaStream_t s) {
+    validate(f, nt, ns);
+    c->have_state = false;
+    c->kspec = ks;
+    c->cfg = f;
+    c->dim = ks.out_dim();
+    c->cheb = make_cheb(f.degree);
+    const int n0 = f.resolved_n0();
+    cudaEvent_t* ev = c->ev;
+
+    CSFS_CK(cudaEventRecord(ev[0], s));
+    c->shared = (nt == ns) && device_equal(txyz, sxyz, nt * 3 * sizeof(double), c->sc, s);
+    DeviceTree& T = c->ttree;
+    DeviceTree& S = c->shared ? c->ttree : c->stree;
+    build_tree(T, c->sc, txyz, c->shared ? sw : nullptr, (long long)nt, f.degree, n0, f.shrink,
+               c->cheb, s);
+    if (!c->shared) build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s);
+    CSFS_CK(cudaEventRecord(ev[1], s));
+
+    upward_pass(S, c->cheb, s);
+    CSFS_CK(cudaEventRecord(ev[2], s));
+
+    dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
+    build_items(T, S, c->lists, c->items, c->sc, s);
+    CSFS_CK(cudaEventRecord(ev[3], s));
+
+    const int dim = c->dim;
+    c->phi_near.grow(nt * dim);
+    T.qphi.grow(size_t(T.ncl) * T.npp * dim);
+    CSFS_CK(cudaMemsetAsync(c->phi_near.p, 0, nt * dim * sizeof(double), s));
+    CSFS_CK(cudaMemsetAsync(T.qphi.p, 0, size_t(T.ncl) * T.npp * dim * sizeof(double), s));
+    c->counter.grow(4);
+    interact(ks, T, S, c->items, c->phi_near, c->counter, s);
+    CSFS_CK(cudaEventRecord(ev[4], s));
+
+    downward_pass(T, c->cheb, dim, c->phi_near, out, s);
+    CSFS_CK(cudaEventRecord(ev[5], s));
+    CSFS_CK(cudaEventSynchronize(ev[5]));
+    c->have_state = true;
+
+    if (st) {
+        std::memset(st, 0, sizeof(*st));
+        st->t_tree_build = ev_ms(ev[0], ev[1]) * 1e-3;
+        st->t_upward = ev_ms(ev[1], ev[2]) * 1e-3;
+        st->t_traversal = ev_ms(ev[2], ev[4]) * 1e-3;
+        st->t_lists = ev_ms(ev[2], ev[3]) * 1e-3;
+        st->t_interact = ev_ms(ev[3], ev[4]) * 1e-3;
+        st->t_downward = ev_ms(ev[4], ev[5]) * 1e-3;
+        st->t_total = ev_ms(ev[0], ev[5]) * 1e-3;
+        st->pp = c->lists.n[0];
+        st->pc = c->lists.n[1];
+        st->cp = c->lists.n[2];
+        st->cc = c->lists.n[3];
+        st->evals_pp = c->items.pair_evals[0];
+        st->evals_pc = c->items.pair_evals[1];
+        st->evals_cp = c->items.pair_evals[2];
+        st->evals_cc = c->items.pair_evals[3];
+        st->tgt_depth = T.depth_max();
+        st->tgt_clusters = T.ncl;
+        st->tgt_leaves = T.ncl - count_internal(T);
+        st->src_depth = S.depth_max();
+        st->src_clusters = S.ncl;
+        st->src_leaves = c->shared ? st->tgt_leaves : S.ncl - count_internal(S);
+        st->shared_tree = c->shared ? 1 : 0;
+    }
+}
+
+cudaStream_t pick(csfs_b200_ctx* c, void* stream) {
+    return stream ? static_cast<cudaStream_t>(stream) : c->own;
+}
+
+struct HostTree {
+    std::vector<int> face, depth, begin, end, parent, nchild, ref, inv;
+    std::vector<int4> child;
+};
+
+HostTree fetch_topology(const DeviceTree& t) {
+    HostTree h;
+    const int n = t.ncl;
+    auto get = [&](std::vector<int>& v, const int* p) {
+        v.resize(n);
+        CSFS_CK(cudaMemcpy(v.data(), p, n * sizeof(int), cudaMemcpyDeviceToHost));
+    };
+    get(h.face, t.face);
+    get(h.depth, t.depth);
+    get(h.begin, t.begin);
+    get(h.end, t.end);
+    get(h.parent, t.parent);
+    get(h.nchild, t.nchild);
+    h.child.resize(n);
+    CSFS_CK(cudaMemcpy(h.child.data(), t.child.p, n * sizeof(int4), cudaMemcpyDeviceToHost));
+    h.ref = reference_ids(h.parent, h.depth, h.child, h.nchild);
+    h.inv.assign(n, -1);
+    for (int i = 0; i < n; ++i) h.inv[h.ref[i]] = i;
+    return h;
+}
+
+const DeviceTree& which_tree(const csfs_b200_ctx* c, int which) {
+    if (!c->have_state) throw InvalidArgument("no csfmm state: call csfs_b200_csfmm first");
+    if (which != 0 && which != 1) throw InvalidArgument("which must be 0 (target) or 1 (source)");
+    return (which == 0 || c->shared) ? c->ttree : c->stree;
+}
+
+}  // namespace
+
+extern "C" {
+
+int csfs_b200_create(csfs_b200_ctx** out, int device) {
+    if (!out) return CSFS_B200_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto c = std::make_unique<csfs_b200_ctx>();
+    c->device = device;
+    int rc = guarded(c.get(), [&] {
+        int count = 0;
+        CSFS_CK(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) throw InvalidArgument("no CUDA device " + std::to_string(device));
+        cudaDeviceProp prop{};
+        CSFS_CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            throw CudaFailure("csfs_b200 is built for sm_100a; device " + std::to_string(device) +
+                              " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+        CSFS_CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+        for (auto& e : c->ev) CSFS_CK(cudaEventCreate(&e));
+        CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
+    });
+    if (rc != CSFS_B200_OK) {
+        // keep the context alive only to report the error? The caller gets NULL.
+        return rc;
+    }
+    *out = c.release();
+    return CSFS_B200_OK;
+}
+
+void csfs_b200_destroy(csfs_b200_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->own) cudaStreamSynchronize(c->own);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->sc.host) cudaFreeHost(c->sc.host);
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+}
+
+const char* csfs_b200_last_error(const csfs_b200_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int csfs_b200_csfmm_device(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
+                           const double* sw, size_t ns, const csfs_b200_kernel* k,
+                           const csfs_b200_config* cfg, double* out, csfs_b200_stats* st,
+                           void* stream) {
+    return guarded(c, [&] {
+        run_csfmm(c, txyz, nt, sxyz, sw, ns, to_spec(k), to_cfg(cfg), out, st, pick(c, stream));
+    });
+}
+
+int csfs_b200_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
+                    const double* sw, size_t ns, const csfs_b200_kernel* k,
+                    const csfs_b200_config* cfg, double* out, csfs_b200_stats* st) {
+    return guarded(c, [&] {
+        const KernelSpec ks = to_spec(k);
+        const FmmConfig f = to_cfg(cfg);
+        validate(f, nt, ns);
+        cudaStream_t s = c->own;
+        const bool same = (txyz == sxyz && nt == ns);
+        c->h_txyz.grow(nt * 3);
+        CSFS_CK(cudaMemcpyAsync(c->h_txyz.p, txyz, nt * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        const double* dsrc = c->h_txyz.p;
+        if (!same) {
+            c->h_sxyz.grow(ns * 3);
+            CSFS_CK(cudaMemcpyAsync(c->h_sxyz.p, sxyz, ns * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+            dsrc = c->h_sxyz.p;
+        }
+        c->h_w.grow(ns);
+        CSFS_CK(cudaMemcpyAsync(c->h_w.p, sw, ns * sizeof(double), cudaMemcpyHostToDevice, s));
+        const size_t nout = nt * size_t(ks.out_dim());
+        c->h_out.grow(nout);
+        run_csfmm(c, c->h_txyz.p, nt, dsrc, c->h_w.p, ns, ks, f, c->h_out.p, st, s);
+        CSFS_CK(cudaMemcpyAsync(out, c->h_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
+    });
+}
+
+int csfs_b200_direct_device(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
+                            const double* sw, size_t ns, const csfs_b200_kernel* k, double* out,
+                            void* stream) {
+    return guarded(c, [&] {
+        const KernelSpec ks = to_spec(k);
+        c->counter.grow(4);
+        direct_allpairs(ks, txyz, (long long)nt, sxyz, sw, (long long)ns, out, c->d_soa, c->d_items,
+                        c->d_segs, c->counter, pick(c, stream));
+    });
+}
+
+int csfs_b200_direct(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
+                     const double* sw, size_t ns, const csfs_b200_kernel* k, double* out) {
+    return guarded(c, [&] {
+        const KernelSpec ks = to_spec(k);
+        cudaStream_t s = c->own;
+        c->h_txyz.grow(std::max<size_t>(nt * 3, 1));
+        c->h_sxyz.grow(std::max<size_t>(ns * 3, 1));
+        c->h_w.grow(std::max<size_t>(ns, 1));
+        const size_t nout = nt * size_t(ks.out_dim());
+        c->h_out.grow(std::max<size_t>(nout, 1));
+        if (nt) CSFS_CK(cudaMemcpyAsync(c->h_txyz.p, txyz, nt * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        if (ns) {
+            CSFS_CK(cudaMemcpyAsync(c->h_sxyz.p, sxyz, ns * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+            CSFS_CK(cudaMemcpyAsync(c->h_w.p, sw, ns * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        if (nout) CSFS_CK(cudaMemsetAsync(c->h_out.p, 0, nout * sizeof(double), s));
+        c->counter.grow(4);
+        direct_allpairs(ks, c->h_txyz.p, (long long)nt, c->h_sxyz.p, c->h_w.p, (long long)ns, c->h_out.p,
+                        c->d_soa, c->d_items, c->d_segs, c->counter, s);
+        if (nout) CSFS_CK(cudaMemcpyAsync(out, c->h_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
+    });
+}
+
+int csfs_b200_tree_info(const csfs_b200_ctx* c, int which, int* ncl, int* depth, size_t* n, int* npp) {
+    if (!c) return CSFS_B200_INVALID_ARGUMENT;
+    if (!c->have_state || (which != 0 && which != 1)) return CSFS_B200_INVALID_ARGUMENT;
+    const DeviceTree& t = (which == 0 || c->shared) ? c->ttree : c->stree;
+    if (ncl) *ncl = t.ncl;
+    if (depth) *depth = t.depth_max();
+    if (n) *n = size_t(t.n);
+    if (npp) *npp = t.npp;
+    return CSFS_B200_OK;
+}
+
+int csfs_b200_tree_export(csfs_b200_ctx* c, int which, int* perm, int* ints, double* dbls, double* proxy) {
+    return guarded(c, [&] {
+        const DeviceTree& t = which_tree(c, which);
+        const HostTree h = fetch_topology(t);
+        const int n = t.ncl;
+        if (perm) CSFS_CK(cudaMemcpy(perm, t.perm.p, t.n * sizeof(int), cudaMemcpyDeviceToHost));
+        if (ints) {
+            for (int i = 0; i < n; ++i) {
+                int* r = ints + 10 * h.ref[i];
+                r[0] = h.face[i];
+                r[1] = h.begin[i];
+                r[2] = h.end[i];
+                r[3] = h.parent[i] < 0 ? -1 : h.ref[h.parent[i]];
+                r[4] = h.depth[i];
+                r[5] = h.nchild[i];
+                const int cs[4] = {h.child[i].x, h.child[i].y, h.child[i].z, h.child[i].w};
+                for (int q = 0; q < 4; ++q) r[6 + q] = (q < h.nchild[i]) ? h.ref[cs[q]] : -1;
+            }
+        }
+        if (dbls) {
+            const double* src[8] = {t.xi0, t.xi1, t.eta0, t.eta1, t.cx, t.cy, t.cz, t.rad};
+            std::vector<double> col(n);
+            for (int f = 0; f < 8; ++f) {
+                CSFS_CK(cudaMemcpy(col.data(), src[f], n * sizeof(double), cudaMemcpyDeviceToHost));
+                for (int i = 0; i < n; ++i) dbls[8 * h.ref[i] + f] = col[i];
+            }
+        }
+        if (proxy) {
+            const size_t nq = size_t(n) * t.npp;
+            std::vector<double> q[3];
+            const double* src[3] = {t.qx, t.qy, t.qz};
+            for (int f = 0; f < 3; ++f) {
+                q[f].resize(nq);
+                CSFS_CK(cudaMemcpy(q[f].data(), src[f], nq * sizeof(double), cudaMemcpyDeviceToHost));
+            }
+            for (int i = 0; i < n; ++i)
+                for (int k = 0; k < t.npp; ++k)
+                    for (int f = 0; f < 3; ++f)
+                        proxy[(size_t(h.ref[i]) * t.npp + k) * 3 + f] = q[f][size_t(i) * t.npp + k];
+        }
+    });
+}
+
+int csfs_b200_lists_export(csfs_b200_ctx* c, long long* counts, int* pp, int* pc, int* cp, int* cc) {
+    return guarded(c, [&] {
+        if (!c->have_state) throw InvalidArgument("no csfmm state: call csfs_b200_csfmm first");
+        const HostTree ht = fetch_topology(c->ttree);
+        const HostTree hs = c->shared ? ht : fetch_topology(c->stree);
+        int* outs[4] = {pp, pc, cp, cc};
+        for (int k = 0; k < 4; ++k) {
+            if (counts) counts[k] = c->lists.n[k];
+            if (!outs[k]) continue;
+            std::vector<int2> v(c->lists.n[k]);
+            if (!v.empty())
+                CSFS_CK(cudaMemcpy(v.data(), c->lists.l[k].p, v.size() * sizeof(int2), cudaMemcpyDeviceToHost));
+            std::vector<std::pair<int, int>> r(v.size());
+            for (size_t e = 0; e < v.size(); ++e) r[e] = {ht.ref[v[e].x], hs.ref[v[e].y]};
+            std::sort(r.begin(), r.end());
+            for (size_t e = 0; e < r.size(); ++e) {
+                outs[k][2 * e] = r[e].first;
+                outs[k][2 * e + 1] = r[e].second;
+            }
+        }
+    });
+}
+
+int csfs_b200_proxy_weights_export(csfs_b200_ctx* c, double* pw) {
+    return guarded(c, [&] {
+        const DeviceTree& s = which_tree(c, 1);
+        const HostTree h = fetch_topology(s);
+        const size_t nq = size_t(s.ncl) * s.npp;
+        std::vector<double> q(nq);
+        CSFS_CK(cudaMemcpy(q.data(), s.qw.p, nq * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < s.ncl; ++i)
+            std::memcpy(pw + size_t(h.ref[i]) * s.npp, q.data() + size_t(i) * s.npp, s.npp * sizeof(double));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,178 @@
+// Host-side engine structures of the B200 CSFMM: device buffers, the device-resident
+// cluster tree (the GPU analogue of csfs::ClusterTree, cluster_tree.hpp:52-67), the
+// interaction lists (summation.hpp:55-59) and the work items the evaluation kernel
+// consumes.  One Engine per csfs_b200_ctx; one device per Engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace csfs_b200 {
+
+// Grow-only device buffer.  grow() discards contents, grow_keep() preserves them.
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void grow(size_t n) {
+        if (n <= cap) return;
+        if (p) CSFS_CK(cudaFree(p));
+        p = nullptr;
+        const size_t c = n + n / 4 + 64;
+        CSFS_CK(cudaMalloc(&p, c * sizeof(T)));
+        cap = c;
+    }
+    void grow_keep(size_t n, size_t used, cudaStream_t s) {
+        if (n <= cap) return;
+        const size_t c = n + n / 2 + 64;
+        T* q = nullptr;
+        CSFS_CK(cudaMalloc(&q, c * sizeof(T)));
+        if (p && used) CSFS_CK(cudaMemcpyAsync(q, p, used * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        if (p) {
+            CSFS_CK(cudaStreamSynchronize(s));
+            CSFS_CK(cudaFree(p));
+        }
+        p = q;
+        cap = c;
+    }
+    operator T*() const { return p; }
+};
+
+// Raw-pointer view of a tree, passed by value into kernels.
+struct TreeView {
+    long long n;
+    int np, npp;
+    // particles, tree order
+    const double *px, *py, *pz, *xi, *eta, *w;
+    const int *perm, *node;
+    // clusters (internal, level-major ids)
+    const int *face, *depth, *begin, *end, *parent, *nchild;
+    const int4* child;
+    const double *xi0, *xi1, *eta0, *eta1, *cx, *cy, *cz, *rad;
+    // proxies: cluster c owns [c*npp, (c+1)*npp), index k1*np+k2 (interpolation.cpp:64-67)
+    const double *qx, *qy, *qz;
+};
+
+struct DeviceTree {
+    long long n = 0;
+    int degree = 0, np = 0, npp = 0, n0 = 0;
+    bool shrink = true, has_w = false;
+    // particles (tree order) + one scratch copy for the partition scatters
+    DevBuf<double> px, py, pz, xi, eta, w;
+    DevBuf<int> perm, node;
+    DevBuf<double> px2, py2, pz2, xi2, eta2, w2;
+    DevBuf<int> perm2, node2, rank;
+    // clusters
+    int ncl = 0, cap = 0;
+    DevBuf<int> face, depth, begin, end, parent, nchild;
+    DevBuf<int4> child;
+    DevBuf<double> xi0, xi1, eta0, eta1, cx, cy, cz, rad;
+    DevBuf<unsigned char> split;
+    DevBuf<unsigned long long> bnd;  // 4 per cluster: min xi, max xi, min eta, max eta (ordered)
+    std::vector<int> level_first, level_count;
+    std::vector<int> root_count;  // 6
+    // proxies
+    DevBuf<double> qx, qy, qz;
+    DevBuf<double> qw;    // proxy weights (source side), ncl*npp
+    DevBuf<double> qphi;  // proxy potentials (target side), ncl*npp*dim
+
+    void reserve_clusters(int n_needed, cudaStream_t s);
+    TreeView view() const;
+    int depth_max() const { return int(level_first.size()) - 1; }
+};
+
+// Scratch shared by the build / traversal phases.
+struct Scratch {
+    DevBuf<int> tiles;      // scan tile totals
+    DevBuf<int> grand;      // scan grand totals (device)
+    DevBuf<int> segP, segE, kid, koff;  // per frontier cluster x 4
+    DevBuf<int> counters;   // misc device counters
+    int* host = nullptr;    // pinned host mirror for small read-backs
+    DevBuf<double> fxi, feta;  // level-0 face coordinates in input order
+    DevBuf<int> fface;
+};
+
+// Interaction lists in internal cluster ids, (t, s) pairs, canonical after build.
+struct Lists {
+    DevBuf<int2> l[4];  // pp, pc, cp, cc
+    long long n[4] = {0, 0, 0, 0};
+    DevBuf<int2> front, front2;
+};
+
+// Work items for the unified evaluation kernel: one item per target leaf (PP+PC
+// sources, targets = leaf particles) and one per target cluster (CP+CC sources,
+// targets = its proxy points).  seg = {start, len}; len < 0 marks a proxy segment.
+struct Items {
+    DevBuf<int> cnt, off, cur;  // per key (2*ncl_t)
+    DevBuf<int> keys;           // non-empty keys, in key order
+    DevBuf<long long> code;     // per entry sort code
+    DevBuf<int2> seg;           // per entry source segment
+    DevBuf<int4> item;          // {tgt_start, tgt_len (neg = proxy), seg_begin, seg_end}
+    DevBuf<unsigned long long> pairs;  // 4 pair-eval counters (pp, pc, cp, cc)
+    int n_items = 0;
+    long long n_entries = 0;
+    unsigned long long pair_evals[4] = {0, 0, 0, 0};
+};
+
+struct KernelSpec {
+    int kind = 0;  // 0 laplace, 1 biharmonic, 2 biot_savart, 3 sal  (KernelKind order)
+    double a1 = -2.7, b0 = -6.21196, b1 = 6.1, rho_ratio = 1025.0 / 5517.0;  // kernels.hpp:18-23
+    int out_dim() const { return kind == 2 ? 3 : 1; }
+};
+
+struct FmmConfig {
+    double mac = 0.7;
+    int degree = 6;
+    int n0 = -1;
+    bool shrink = true;
+    int resolved_n0() const { return n0 >= 0 ? n0 : 4 * degree * degree; }
+};
+
+struct PhaseTimes {
+    double tree = 0, upward = 0, traversal = 0, lists = 0, interact = 0, downward = 0, total = 0;
+};
+
+// --- phase entry points (implemented in the .cu files) -------------------------------
+
+// tree.cu: builds `tree` from AoS xyz (device, input order) and optional weights.
+void build_tree(DeviceTree& tree, Scratch& sc, const double* xyz, const double* w, long long n,
+                int degree, int n0, bool shrink, const Cheb& cheb, cudaStream_t s);
+// Device byte comparison (targets == sources detection).
+bool device_equal(const void* a, const void* b, size_t bytes, Scratch& sc, cudaStream_t s);
+
+// passes.cu
+void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s);
+void downward_pass(DeviceTree& tgt, const Cheb& cheb, int dim, const double* phi_near, double* out,
+                   cudaStream_t s);
+
+// traverse.cu
+void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, int n0, Lists& lists,
+                    Scratch& sc, cudaStream_t s);
+void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& lists, Items& items,
+                 Scratch& sc, cudaStream_t s);
+
+// interact.cu
+void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, const Items& items,
+              double* phi_near, int* work_counter, cudaStream_t s);
+// all-pairs (direct_sum, summation.cpp:136-161): targets/sources AoS in input order.
+void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, const double* sxyz,
+                     const double* sw, long long ns, double* out, DevBuf<double>& soa,
+                     DevBuf<int4>& items, DevBuf<int2>& segs, int* work_counter, cudaStream_t s);
+
+// reference cluster ids (LIFO expansion order, cluster_tree.cpp:87-140) for export.
+std::vector<int> reference_ids(const std::vector<int>& parent, const std::vector<int>& depth,
+                               const std::vector<int4>& child, const std::vector<int>& nchild);
+
+}  // namespace csfs_b200

@@ -1,0 +1,228 @@
+// Upward (P2M + M2M) and downward (L2L + L2P) passes: the B200 restatement of
+// upward_pass / downward_pass (/root/reference/proj/src/cluster_tree.cpp:163-220, 228-283)
+// and transfer_matrix (:16-25).
+//
+// These are HBM/latency-bound tensor-product barycentric contractions over (p+1)^2
+// Chebyshev-2 proxy grids (K7, K8, K12, K13 in SURVEY.md §2.3).  One CTA per cluster;
+// the per-particle 1-D bases live in shared memory, every output coefficient is owned by
+// exactly one thread (deterministic, no atomics).  The leaf P2M keeps the reference's
+// accumulation order (particles ascending, a = w*Lx[k1], += a*Ly[k2]) with unfused
+// arithmetic; L2L is done separably (roundoff-level difference).
+#include <algorithm>
+
+#include "engine.hpp"
+
+namespace csfs_b200 {
+
+namespace {
+
+constexpr int kPassThreads = 128;
+constexpr int kP2mChunk = 64;
+
+// Leaf P2M (cluster_tree.cpp:180-191).  Internal clusters are written by k_m2m.
+__global__ void __launch_bounds__(kPassThreads)
+    k_p2m(TreeView t, Cheb cheb, const double* __restrict__ w, double* __restrict__ qw) {
+    extern __shared__ double sm[];
+    const int c = blockIdx.x;
+    if (t.nchild[c] > 0) return;
+    const int np = cheb.np, npp = np * np;
+    double* WL = sm;                    // kP2mChunk x np   (w * Lx)
+    double* LY = sm + kP2mChunk * np;   // kP2mChunk x np
+    const int b = t.begin[c], e = t.end[c];
+    const double x0 = t.xi0[c], x1 = t.xi1[c], e0 = t.eta0[c], e1 = t.eta1[c];
+    const double xm = __dmul_rn(0.5, __dadd_rn(x0, x1)), xh = __dmul_rn(0.5, __dsub_rn(x1, x0));
+    const double em = __dmul_rn(0.5, __dadd_rn(e0, e1)), eh = __dmul_rn(0.5, __dsub_rn(e1, e0));
+    double acc[(kMaxNp * kMaxNp + kPassThreads - 1) / kPassThreads];
+#pragma unroll
+    for (int i = 0; i < (kMaxNp * kMaxNp + kPassThreads - 1) / kPassThreads; ++i) acc[i] = 0.0;
+    for (int base = b; base < e; base += kP2mChunk) {
+        const int m = min(kP2mChunk, e - base);
+        if (threadIdx.x < m) {
+            const int p = base + threadIdx.x;
+            double* wl = WL + threadIdx.x * np;
+            double* ly = LY + threadIdx.x * np;
+            bary1d(cheb, ref_coord(t.xi[p], xm, xh), wl);
+            bary1d(cheb, ref_coord(t.eta[p], em, eh), ly);
+            const double wt = w[p];
+            for (int k = 0; k < np; ++k) wl[k] = __dmul_rn(wt, wl[k]);
+        }
+        __syncthreads();
+        int idx = 0;
+        for (int o = threadIdx.x; o < npp; o += kPassThreads, ++idx) {
+            const int k1 = o / np, k2 = o % np;
+            double a = acc[idx];
+            for (int j = 0; j < m; ++j) a = __dadd_rn(a, __dmul_rn(WL[j * np + k1], LY[j * np + k2]));
+            acc[idx] = a;
+        }
+        __syncthreads();
+    }
+    int idx = 0;
+    for (int o = threadIdx.x; o < npp; o += kPassThreads, ++idx) qw[(long long)c * npp + o] = acc[idx];
+}
+
+// Transfer matrix columns: At[m*np + k] = L^parent_k(child node m)  (transfer_matrix, :16-25).
+__device__ void transfer_cols(const Cheb& cheb, double pmid, double phalf, double cmid,
+                              double chalf, int m, double* At) {
+    const double node = __dadd_rn(cmid, __dmul_rn(chalf, cheb.nodes[m]));
+    const double xhat = phalf > 0.0 ? __ddiv_rn(__dsub_rn(node, pmid), phalf) : 0.0;
+    bary1d(cheb, xhat, At + m * cheb.np);
+}
+
+__device__ __forceinline__ void mid_half(double a0, double a1, double& mid, double& half) {
+    mid = __dmul_rn(0.5, __dadd_rn(a0, a1));
+    half = __dmul_rn(0.5, __dsub_rn(a1, a0));
+}
+
+// M2M (cluster_tree.cpp:192-216): pw = sum_children Axi * cw * Aeta^T, for one level.
+__global__ void __launch_bounds__(kPassThreads)
+    k_m2m(TreeView t, Cheb cheb, int first, double* __restrict__ qw) {
+    extern __shared__ double sm[];
+    const int c = first + blockIdx.x;
+    const int nch = t.nchild[c];
+    if (nch == 0) return;
+    const int np = cheb.np, npp = np * np;
+    double* Ax = sm;             // At layout
+    double* Ae = sm + npp;
+    double* tmp = sm + 2 * npp;  // tmp[k1*np + m2]
+    double pxm, pxh, pem, peh;
+    mid_half(t.xi0[c], t.xi1[c], pxm, pxh);
+    mid_half(t.eta0[c], t.eta1[c], pem, peh);
+    double acc[(kMaxNp * kMaxNp + kPassThreads - 1) / kPassThreads];
+#pragma unroll
+    for (int i = 0; i < (kMaxNp * kMaxNp + kPassThreads - 1) / kPassThreads; ++i) acc[i] = 0.0;
+    const int4 ch4 = t.child[c];
+    const int chs[4] = {ch4.x, ch4.y, ch4.z, ch4.w};
+    for (int q = 0; q < nch; ++q) {
+        const int ch = chs[q];
+        double cxm, cxh, cem, ceh;
+        mid_half(t.xi0[ch], t.xi1[ch], cxm, cxh);
+        mid_half(t.eta0[ch], t.eta1[ch], cem, ceh);
+        if (threadIdx.x < np) transfer_cols(cheb, pxm, pxh, cxm, cxh, threadIdx.x, Ax);
+        else if (threadIdx.x < 2 * np) transfer_cols(cheb, pem, peh, cem, ceh, threadIdx.x - np, Ae);
+        __syncthreads();
+        const double* cw = qw + (long long)ch * npp;
+        for (int o = threadIdx.x; o < npp; o += kPassThreads) {
+            const int k1 = o / np, m2 = o % np;
+            double s = 0.0;
+            for (int m1 = 0; m1 < np; ++m1) s = __dadd_rn(s, __dmul_rn(Ax[m1 * np + k1], cw[m1 * np + m2]));
+            tmp[o] = s;
+        }
+        __syncthreads();
+        int idx = 0;
+        for (int o = threadIdx.x; o < npp; o += kPassThreads, ++idx) {
+            const int k1 = o / np, k2 = o % np;
+            double s = 0.0;
+            for (int m2 = 0; m2 < np; ++m2) s = __dadd_rn(s, __dmul_rn(tmp[k1 * np + m2], Ae[m2 * np + k2]));
+            acc[idx] = __dadd_rn(acc[idx], s);
+        }
+        __syncthreads();
+    }
+    int idx = 0;
+    for (int o = threadIdx.x; o < npp; o += kPassThreads, ++idx) qw[(long long)c * npp + o] = acc[idx];
+}
+
+// L2L (cluster_tree.cpp:256-279), one CTA per child at level `first..`:
+// child[n1,n2,d] += sum_{m1,m2} Axi[m1,n1] Aeta[m2,n2] P[m1,m2,d], done separably.
+__global__ void __launch_bounds__(kPassThreads)
+    k_l2l(TreeView t, Cheb cheb, int first, int dim, double* __restrict__ qphi) {
+    extern __shared__ double sm[];
+    const int ch = first + blockIdx.x;
+    const int c = t.parent[ch];
+    if (c < 0) return;
+    const int np = cheb.np, npp = np * np;
+    double* Ax = sm;
+    double* Ae = sm + npp;
+    double* tmp = sm + 2 * npp;  // tmp[(n1*np + m2)*dim + d]
+    double pxm, pxh, pem, peh, cxm, cxh, cem, ceh;
+    mid_half(t.xi0[c], t.xi1[c], pxm, pxh);
+    mid_half(t.eta0[c], t.eta1[c], pem, peh);
+    mid_half(t.xi0[ch], t.xi1[ch], cxm, cxh);
+    mid_half(t.eta0[ch], t.eta1[ch], cem, ceh);
+    if (threadIdx.x < np) transfer_cols(cheb, pxm, pxh, cxm, cxh, threadIdx.x, Ax);
+    else if (threadIdx.x < 2 * np) transfer_cols(cheb, pem, peh, cem, ceh, threadIdx.x - np, Ae);
+    __syncthreads();
+    const double* P = qphi + (long long)c * npp * dim;
+    for (int o = threadIdx.x; o < npp * dim; o += kPassThreads) {
+        const int d = o % dim, r = o / dim, n1 = r / np, m2 = r % np;
+        double s = 0.0;
+        // Axi[m1][n1] = L^parent_{m1}(child node n1) = At[n1*np + m1]
+        for (int m1 = 0; m1 < np; ++m1) s += Ax[n1 * np + m1] * P[(m1 * np + m2) * dim + d];
+        tmp[o] = s;
+    }
+    __syncthreads();
+    double* C = qphi + (long long)ch * npp * dim;
+    for (int o = threadIdx.x; o < npp * dim; o += kPassThreads) {
+        const int d = o % dim, r = o / dim, n1 = r / np, n2 = r % np;
+        double s = 0.0;
+        for (int m2 = 0; m2 < np; ++m2) s += Ae[n2 * np + m2] * tmp[(n1 * np + m2) * dim + d];
+        C[o] += s;
+    }
+}
+
+// L2P (cluster_tree.cpp:241-255) fused with the final scatter to input order:
+// out[perm[t]] = near[t] + sum_k Lx[k1] Ly[k2] P[k].
+__global__ void __launch_bounds__(kPassThreads)
+    k_l2p(TreeView t, Cheb cheb, int dim, const double* __restrict__ qphi,
+          const double* __restrict__ near, double* __restrict__ out) {
+    extern __shared__ double sm[];
+    const int c = blockIdx.x;
+    if (t.nchild[c] > 0) return;
+    const int b = t.begin[c], e = t.end[c];
+    if (b == e) return;
+    const int np = cheb.np, npp = np * np;
+    for (int o = threadIdx.x; o < npp * dim; o += kPassThreads) sm[o] = qphi[(long long)c * npp * dim + o];
+    __syncthreads();
+    double xm, xh, em, eh;
+    mid_half(t.xi0[c], t.xi1[c], xm, xh);
+    mid_half(t.eta0[c], t.eta1[c], em, eh);
+    for (int p = b + threadIdx.x; p < e; p += kPassThreads) {
+        double lx[kMaxNp], ly[kMaxNp];
+        bary1d(cheb, ref_coord(t.xi[p], xm, xh), lx);
+        bary1d(cheb, ref_coord(t.eta[p], em, eh), ly);
+        double f[3] = {0.0, 0.0, 0.0};
+        for (int k1 = 0; k1 < np; ++k1) {
+            const double a = lx[k1];
+            const double* row = sm + k1 * np * dim;
+            for (int k2 = 0; k2 < np; ++k2) {
+                const double bb = a * ly[k2];
+                for (int d = 0; d < dim; ++d) f[d] += bb * row[k2 * dim + d];
+            }
+        }
+        const long long dst = (long long)t.perm[p] * dim;
+        for (int d = 0; d < dim; ++d) out[dst + d] = near[(long long)p * dim + d] + f[d];
+    }
+}
+
+}  // namespace
+
+void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s) {
+    const TreeView v = src.view();
+    const int np = cheb.np, npp = np * np;
+    src.qw.grow((size_t)src.ncl * npp);
+    const size_t sm_p2m = size_t(2) * kP2mChunk * np * sizeof(double);
+    k_p2m<<<src.ncl, kPassThreads, sm_p2m, s>>>(v, cheb, src.w, src.qw);
+    CSFS_LAUNCH_CHECK();
+    const size_t sm_m2m = size_t(3) * npp * sizeof(double);
+    for (int L = src.depth_max() - 1; L >= 0; --L) {
+        if (src.level_count[L] == 0) continue;
+        k_m2m<<<src.level_count[L], kPassThreads, sm_m2m, s>>>(v, cheb, src.level_first[L], src.qw);
+        CSFS_LAUNCH_CHECK();
+    }
+}
+
+void downward_pass(DeviceTree& tgt, const Cheb& cheb, int dim, const double* phi_near, double* out,
+                   cudaStream_t s) {
+    const TreeView v = tgt.view();
+    const int np = cheb.np, npp = np * np;
+    const size_t sm_l2l = size_t(2 * npp + npp * dim) * sizeof(double);
+    for (int L = 1; L <= tgt.depth_max(); ++L) {
+        if (tgt.level_count[L] == 0) continue;
+        k_l2l<<<tgt.level_count[L], kPassThreads, sm_l2l, s>>>(v, cheb, tgt.level_first[L], dim, tgt.qphi);
+        CSFS_LAUNCH_CHECK();
+    }
+    const size_t sm_l2p = size_t(npp) * dim * sizeof(double);
+    k_l2p<<<tgt.ncl, kPassThreads, sm_l2p, s>>>(v, cheb, dim, tgt.qphi, phi_near, out);
+    CSFS_LAUNCH_CHECK();
+}
+
+}  // namespace csfs_b200

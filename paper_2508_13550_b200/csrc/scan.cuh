@@ -1,0 +1,156 @@
+// Multi-counter exclusive scan / stream compaction, the primitive behind the stable
+// face bucketing and the stable 4-way quadrant partitions of the tree build
+// (cluster_tree.cpp:38-41, :102-122) and the frontier compaction of the dual tree
+// traversal (summation.cpp:163-203).
+//
+// Three launches: (1) per-tile totals of K counters, (2) one CTA scans the tile
+// totals, (3) per-element exclusive prefixes are rebuilt inside each tile and handed to
+// an emitter.  Tiles are 1024 elements (256 threads x 4 consecutive items), so each
+// warp touches a contiguous 128-element span: coalesced for 4/8-byte payloads.
+// Counts are deterministic (no atomics), hence every consumer is order-stable.
+#pragma once
+
+#include "common.cuh"
+
+namespace csfs_b200 {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <int K>
+__device__ __forceinline__ void block_exclusive_scan(int (&v)[K], int (&total)[K]) {
+    __shared__ int warp_tot[kScanThreads / 32][K];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        int x = v[k];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        incl[k] = x;
+    }
+    if (lane == 31)
+#pragma unroll
+        for (int k = 0; k < K; ++k) warp_tot[warp][k] = incl[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        int pre = 0, tot = 0;
+        for (int w = 0; w < kScanThreads / 32; ++w) {
+            const int t = warp_tot[w][k];
+            if (w < warp) pre += t;
+            tot += t;
+        }
+        v[k] = pre + incl[k] - v[k];
+        total[k] = tot;
+    }
+    __syncthreads();
+}
+
+// f(i, int c[K]) writes the K counts of element i (c is zeroed before the call).
+template <int K, class F>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_totals(long long n, F f, int* tile_tot) {
+    const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+    int t[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) t[k] = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const long long i = base + j;
+        if (i < n) {
+            int c[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) c[k] = 0;
+            f(i, c);
+#pragma unroll
+            for (int k = 0; k < K; ++k) t[k] += c[k];
+        }
+    }
+    int tot[K];
+    block_exclusive_scan<K>(t, tot);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) tile_tot[(long long)blockIdx.x * K + k] = tot[k];
+}
+
+// One CTA: exclusive scan of the tile totals (in place -> offsets), grand totals out.
+template <int K>
+__global__ void __launch_bounds__(kScanThreads) scan_tiles(int ntiles, int* tile_tot, int* grand) {
+    int carry[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) carry[k] = 0;
+    for (int b0 = 0; b0 < ntiles; b0 += kScanThreads) {
+        const int b = b0 + threadIdx.x;
+        int v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] = b < ntiles ? tile_tot[(long long)b * K + k] : 0;
+        int tot[K];
+        block_exclusive_scan<K>(v, tot);
+        if (b < ntiles)
+#pragma unroll
+            for (int k = 0; k < K; ++k) tile_tot[(long long)b * K + k] = v[k] + carry[k];
+#pragma unroll
+        for (int k = 0; k < K; ++k) carry[k] += tot[k];
+    }
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) grand[k] = carry[k];
+}
+
+// e(i, const int c[K], const int pre[K]): pre = exclusive global prefix of each counter.
+template <int K, class F, class E>
+__global__ void __launch_bounds__(kScanThreads)
+    scan_emit(long long n, F f, const int* tile_off, E e) {
+    const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+    int c[kScanItems][K];
+    int t[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) t[k] = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) c[j][k] = 0;
+        const long long i = base + j;
+        if (i < n) f(i, c[j]);
+#pragma unroll
+        for (int k = 0; k < K; ++k) t[k] += c[j][k];
+    }
+    int tot[K];
+    block_exclusive_scan<K>(t, tot);
+    int pre[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) pre[k] = tile_off[(long long)blockIdx.x * K + k] + t[k];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const long long i = base + j;
+        if (i < n) e(i, c[j], pre);
+#pragma unroll
+        for (int k = 0; k < K; ++k) pre[k] += c[j][k];
+    }
+}
+
+// Host driver: runs the three phases on `stream`.  `tile_buf` must hold
+// ceil(n/1024)*K ints, `grand` K ints (device).  Returns nothing; grand totals stay on
+// the device for the caller to fetch when it needs them.
+template <int K, class F, class E>
+void run_scan(long long n, F f, E e, int* tile_buf, int* grand, cudaStream_t stream) {
+    if (n <= 0) {
+        CSFS_CK(cudaMemsetAsync(grand, 0, K * sizeof(int), stream));
+        return;
+    }
+    const int ntiles = ceil_div(n, kScanTile);
+    scan_tile_totals<K><<<ntiles, kScanThreads, 0, stream>>>(n, f, tile_buf);
+    CSFS_LAUNCH_CHECK();
+    scan_tiles<K><<<1, kScanThreads, 0, stream>>>(ntiles, tile_buf, grand);
+    CSFS_LAUNCH_CHECK();
+    scan_emit<K><<<ntiles, kScanThreads, 0, stream>>>(n, f, tile_buf, e);
+    CSFS_LAUNCH_CHECK();
+}
+
+inline long long scan_tile_ints(long long n, int K) { return (long long)ceil_div(n < 1 ? 1 : n, kScanTile) * K; }
+
+}  // namespace csfs_b200

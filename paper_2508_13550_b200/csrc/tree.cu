@@ -1,0 +1,599 @@
+// GPU cluster-tree build: the B200 restatement of csfs::ClusterTree's constructor
+// (/root/reference/proj/src/cluster_tree.cpp:29-147).
+//
+// The reference builds the quadtree serially with a LIFO stack.  Every split
+// decision only depends on the node's own particles (shrunk bounds -> midpoint ->
+// quadrant -> stable 4-way partition), so the same tree is produced level by level:
+//   level 0 : face_project per particle (K1), stable bucketing by face (K2 = 6-way scan)
+//   level d : for every splitting node, quadrant keys, one global 4-counter scan, a
+//             single-CTA child allocator (children in parent order, empties pruned),
+//             and a scatter that keeps each node's range contiguous (K3)
+//   per level: shrunk bounds, centre and radius by warp-aggregated integer atomics on
+//             order-preserving encodings (exact, so deterministic)   (K4)
+// Internal cluster ids are level-major (BFS); reference_ids() maps them onto the
+// reference's LIFO numbering for export (K5).  Particle data stays SoA in HBM.
+#include <algorithm>
+
+#include "engine.hpp"
+#include "scan.cuh"
+
+namespace csfs_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void k_face(const double* __restrict__ xyz, long long n, int* fface, double* fxi,
+                       double* feta) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int f;
+    double a, b;
+    face_project(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], f, a, b);
+    fface[i] = f;
+    fxi[i] = a;
+    feta[i] = b;
+}
+
+struct ClusterPtrs {
+    int *face, *depth, *begin, *end, *parent, *nchild;
+    int4* child;
+    double *xi0, *xi1, *eta0, *eta1, *cx, *cy, *cz, *rad;
+    unsigned char* split;
+    unsigned long long* bnd;
+};
+
+ClusterPtrs cluster_ptrs(DeviceTree& t) {
+    return {t.face, t.depth, t.begin, t.end, t.parent, t.nchild, t.child, t.xi0, t.xi1,
+            t.eta0, t.eta1, t.cx,    t.cy,    t.cz,  t.rad,    t.split,  t.bnd};
+}
+
+__global__ void k_roots(ClusterPtrs c, const int* grand) {
+    const int k = threadIdx.x;
+    if (k >= 6) return;
+    int b = 0;
+    for (int j = 0; j < k; ++j) b += grand[j];
+    c.face[k] = k;
+    c.depth[k] = 0;
+    c.begin[k] = b;
+    c.end[k] = b + grand[k];
+    c.parent[k] = -1;
+    c.nchild[k] = 0;
+    c.child[k] = make_int4(-1, -1, -1, -1);
+    // face square (cluster_tree.cpp:72)
+    c.xi0[k] = -kPi / 4.0;
+    c.xi1[k] = kPi / 4.0;
+    c.eta0[k] = -kPi / 4.0;
+    c.eta1[k] = kPi / 4.0;
+}
+
+// --- per-level finishing (finish_cluster lambda, cluster_tree.cpp:52-70) ------------------
+
+__global__ void k_bnd_init(int first, const int* nnew_dev, int cnt_host, ClusterPtrs c) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cnt = nnew_dev ? *nnew_dev : cnt_host;
+    if (j >= cnt) return;
+    const int id = first + j;
+    c.bnd[4 * id + 0] = ~0ull;
+    c.bnd[4 * id + 1] = 0ull;
+    c.bnd[4 * id + 2] = ~0ull;
+    c.bnd[4 * id + 3] = 0ull;
+    c.rad[id] = 0.0;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, d);
+        v = o < v ? o : v;
+    }
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, d);
+        v = o > v ? o : v;
+    }
+    return v;
+}
+
+// Shrunk bounds: min/max of xi, eta over each new cluster's particles (:53-61).
+__global__ void k_bounds(long long n, int first, const int* nnew_dev, int cnt_host,
+                         const int* __restrict__ node, const double* __restrict__ xi,
+                         const double* __restrict__ eta, unsigned long long* bnd) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int cnt = nnew_dev ? *nnew_dev : cnt_host;
+    int nd = -1;
+    unsigned long long a = 0, b = 0;
+    if (i < n) {
+        nd = node[i];
+        if (nd >= first && nd < first + cnt) {
+            a = ord_enc(xi[i]);
+            b = ord_enc(eta[i]);
+        } else {
+            nd = -1;
+        }
+    }
+    const int nd0 = __shfl_sync(0xffffffffu, nd, 0);
+    if (__all_sync(0xffffffffu, nd == nd0)) {
+        if (nd0 < 0) return;
+        const unsigned long long amin = warp_min_u64(a), amax = warp_max_u64(a);
+        const unsigned long long bmin = warp_min_u64(b), bmax = warp_max_u64(b);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&bnd[4 * nd0 + 0], amin);
+            atomicMax(&bnd[4 * nd0 + 1], amax);
+            atomicMin(&bnd[4 * nd0 + 2], bmin);
+            atomicMax(&bnd[4 * nd0 + 3], bmax);
+        }
+    } else if (nd >= 0) {
+        atomicMin(&bnd[4 * nd + 0], a);
+        atomicMax(&bnd[4 * nd + 1], a);
+        atomicMin(&bnd[4 * nd + 2], b);
+        atomicMax(&bnd[4 * nd + 3], b);
+    }
+}
+
+// Bounds -> interpolant rectangle, centre (:65-66) and the split decision (:95-96).
+__global__ void k_geom(int first, const int* nnew_dev, int cnt_host, ClusterPtrs c, bool shrink,
+                       int n0, int* nsplit) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cnt = nnew_dev ? *nnew_dev : cnt_host;
+    if (j >= cnt) return;
+    const int id = first + j;
+    const int count = c.end[id] - c.begin[id];
+    double x0 = c.xi0[id], x1 = c.xi1[id], e0 = c.eta0[id], e1 = c.eta1[id];
+    if (shrink && count > 0) {
+        x0 = ord_dec(c.bnd[4 * id + 0]);
+        x1 = ord_dec(c.bnd[4 * id + 1]);
+        e0 = ord_dec(c.bnd[4 * id + 2]);
+        e1 = ord_dec(c.bnd[4 * id + 3]);
+        c.xi0[id] = x0;
+        c.xi1[id] = x1;
+        c.eta0[id] = e0;
+        c.eta1[id] = e1;
+    }
+    const double xm = __dmul_rn(0.5, __dadd_rn(x0, x1));
+    const double em = __dmul_rn(0.5, __dadd_rn(e0, e1));
+    double x, y, z;
+    face_unproject(c.face[id], xm, em, x, y, z);
+    c.cx[id] = x;
+    c.cy[id] = y;
+    c.cz[id] = z;
+    const double ex = __dsub_rn(x1, x0), ey = __dsub_rn(e1, e0);
+    const double ext = (ex < ey) ? ey : ex;  // std::max
+    const bool sp = !(count <= n0 || c.depth[id] >= kMaxDepth) && !(ext < kMinExtent);
+    c.split[id] = sp ? 1 : 0;
+    if (sp) atomicAdd(nsplit, 1);
+}
+
+// Radius = max chordal distance from the centre to the cluster's particles (:67-69).
+__global__ void k_radius(long long n, int first, const int* nnew_dev, int cnt_host,
+                         const int* __restrict__ node, const double* __restrict__ px,
+                         const double* __restrict__ py, const double* __restrict__ pz,
+                         const double* __restrict__ cx, const double* __restrict__ cy,
+                         const double* __restrict__ cz, double* rad) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int cnt = nnew_dev ? *nnew_dev : cnt_host;
+    int nd = -1;
+    unsigned long long r = 0;
+    if (i < n) {
+        nd = node[i];
+        if (nd >= first && nd < first + cnt) {
+            const double dx = __dsub_rn(cx[nd], px[i]);
+            const double dy = __dsub_rn(cy[nd], py[i]);
+            const double dz = __dsub_rn(cz[nd], pz[i]);
+            r = __double_as_longlong(__dsqrt_rn(dot_ref(dx, dy, dz, dx, dy, dz)));
+        } else {
+            nd = -1;
+        }
+    }
+    unsigned long long* radu = reinterpret_cast<unsigned long long*>(rad);
+    const int nd0 = __shfl_sync(0xffffffffu, nd, 0);
+    if (__all_sync(0xffffffffu, nd == nd0)) {
+        if (nd0 < 0) return;
+        const unsigned long long m = warp_max_u64(r);
+        if ((threadIdx.x & 31) == 0) atomicMax(&radu[nd0], m);
+    } else if (nd >= 0) {
+        atomicMax(&radu[nd], r);
+    }
+}
+
+// --- splitting (cluster_tree.cpp:87-141) ------------------------------------------------
+
+__device__ __forceinline__ int quadrant_of(const ClusterPtrs& c, int nd, double x, double e) {
+    const double mx = __dmul_rn(0.5, __dadd_rn(c.xi0[nd], c.xi1[nd]));
+    const double my = __dmul_rn(0.5, __dadd_rn(c.eta0[nd], c.eta1[nd]));
+    return (x >= mx ? 1 : 0) + (e >= my ? 2 : 0);
+}
+
+// Single CTA: children of every splitting frontier node, allocated in frontier order and
+// quadrant order with empty quadrants pruned (:124-140).
+__global__ void __launch_bounds__(kScanThreads)
+    k_children(int first, int cnt, int next_id, ClusterPtrs c, const int* segP, const int* segE,
+               int* kid, int* koff, int* nnew) {
+    int carry = 0;
+    for (int f0 = 0; f0 < cnt; f0 += kScanThreads) {
+        const int f = f0 + threadIdx.x;
+        const int id = first + f;
+        const bool sp = f < cnt && c.split[id];
+        int cntk[4] = {0, 0, 0, 0};
+        int m[1] = {0};
+        if (sp) {
+            for (int k = 0; k < 4; ++k) {
+                cntk[k] = segE[4 * f + k] - segP[4 * f + k];
+                m[0] += cntk[k] > 0;
+            }
+        }
+        int tot[1];
+        block_exclusive_scan<1>(m, tot);
+        if (sp) {
+            int cid = next_id + carry + m[0];
+            int acc = c.begin[id];
+            const double x0 = c.xi0[id], x1 = c.xi1[id], e0 = c.eta0[id], e1 = c.eta1[id];
+            const double mx = __dmul_rn(0.5, __dadd_rn(x0, x1));
+            const double my = __dmul_rn(0.5, __dadd_rn(e0, e1));
+            const double rx0[4] = {x0, mx, x0, mx}, rx1[4] = {mx, x1, mx, x1};
+            const double ry0[4] = {e0, e0, my, my}, ry1[4] = {my, my, e1, e1};
+            int ch[4] = {-1, -1, -1, -1};
+            int nch = 0;
+            const int fc = c.face[id], dp = c.depth[id] + 1;
+            for (int k = 0; k < 4; ++k) {
+                koff[4 * f + k] = acc;
+                kid[4 * f + k] = -1;
+                if (cntk[k] > 0) {
+                    c.face[cid] = fc;
+                    c.depth[cid] = dp;
+                    c.begin[cid] = acc;
+                    c.end[cid] = acc + cntk[k];
+                    c.parent[cid] = id;
+                    c.nchild[cid] = 0;
+                    c.child[cid] = make_int4(-1, -1, -1, -1);
+                    c.xi0[cid] = rx0[k];
+                    c.xi1[cid] = rx1[k];
+                    c.eta0[cid] = ry0[k];
+                    c.eta1[cid] = ry1[k];
+                    kid[4 * f + k] = cid;
+                    ch[nch++] = cid;
+                    ++cid;
+                }
+                acc += cntk[k];
+            }
+            c.child[id] = make_int4(ch[0], ch[1], ch[2], ch[3]);
+            c.nchild[id] = nch;
+        }
+        carry += tot[0];
+    }
+    if (threadIdx.x == 0) *nnew = carry;
+}
+
+struct PartArrays {
+    const double *px, *py, *pz, *xi, *eta, *w;
+    const int *perm, *node;
+    double *px2, *py2, *pz2, *xi2, *eta2, *w2;
+    int *perm2, *node2;
+};
+
+// Stable scatter: moving particles go to koff + rank-within-(node, quadrant), others stay.
+__global__ void k_scatter(long long n, int first, int cnt, ClusterPtrs c, PartArrays a,
+                          const int* __restrict__ rank, const int* __restrict__ segP,
+                          const int* __restrict__ kid, const int* __restrict__ koff) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int nd = a.node[i];
+    long long pos = i;
+    int newnode = nd;
+    const double x = a.xi[i], e = a.eta[i];
+    if (nd >= first && nd < first + cnt && c.split[nd]) {
+        const int q = quadrant_of(c, nd, x, e);
+        const int f = nd - first;
+        pos = koff[4 * f + q] + (rank[i] - segP[4 * f + q]);
+        newnode = kid[4 * f + q];
+    }
+    a.px2[pos] = a.px[i];
+    a.py2[pos] = a.py[i];
+    a.pz2[pos] = a.pz[i];
+    a.xi2[pos] = x;
+    a.eta2[pos] = e;
+    a.perm2[pos] = a.perm[i];
+    a.node2[pos] = newnode;
+    if (a.w) a.w2[pos] = a.w[i];
+}
+
+// Proxy points (interpolation.cpp:51-68): mapped nodes mid + half*s_k, pushed to the sphere.
+__global__ void k_proxy(int ncl, int np, Cheb cheb, const int* __restrict__ face,
+                        const double* __restrict__ xi0, const double* __restrict__ xi1,
+                        const double* __restrict__ eta0, const double* __restrict__ eta1,
+                        double* qx, double* qy, double* qz) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int npp = np * np;
+    if (g >= (long long)ncl * npp) return;
+    const int c = int(g / npp), k = int(g % npp);
+    const int k1 = k / np, k2 = k % np;
+    const double xm = __dmul_rn(0.5, __dadd_rn(xi0[c], xi1[c]));
+    const double xh = __dmul_rn(0.5, __dsub_rn(xi1[c], xi0[c]));
+    const double em = __dmul_rn(0.5, __dadd_rn(eta0[c], eta1[c]));
+    const double eh = __dmul_rn(0.5, __dsub_rn(eta1[c], eta0[c]));
+    const double xn = __dadd_rn(xm, __dmul_rn(xh, cheb.nodes[k1]));
+    const double en = __dadd_rn(em, __dmul_rn(eh, cheb.nodes[k2]));
+    double x, y, z;
+    face_unproject(face[c], xn, en, x, y, z);
+    qx[g] = x;
+    qy[g] = y;
+    qz[g] = z;
+}
+
+__global__ void k_equal(const unsigned long long* a, const unsigned long long* b, long long n,
+                        int* diff) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        if (a[i] != b[i]) {
+            *diff = 1;
+            return;
+        }
+}
+
+void finish_level(DeviceTree& t, Scratch& sc, int first, const int* nnew_dev, int cnt_bound,
+                  cudaStream_t s) {
+    ClusterPtrs c = cluster_ptrs(t);
+    const int gb = ceil_div(std::max(cnt_bound, 1), kThreads);
+    const int gp = ceil_div(t.n, kThreads);
+    k_bnd_init<<<gb, kThreads, 0, s>>>(first, nnew_dev, cnt_bound, c);
+    CSFS_LAUNCH_CHECK();
+    k_bounds<<<gp, kThreads, 0, s>>>(t.n, first, nnew_dev, cnt_bound, t.node, t.xi, t.eta, t.bnd);
+    CSFS_LAUNCH_CHECK();
+    CSFS_CK(cudaMemsetAsync(sc.counters.p + 1, 0, sizeof(int), s));
+    k_geom<<<gb, kThreads, 0, s>>>(first, nnew_dev, cnt_bound, c, t.shrink, t.n0, sc.counters.p + 1);
+    CSFS_LAUNCH_CHECK();
+    k_radius<<<gp, kThreads, 0, s>>>(t.n, first, nnew_dev, cnt_bound, t.node, t.px, t.py, t.pz,
+                                      t.cx, t.cy, t.cz, t.rad);
+    CSFS_LAUNCH_CHECK();
+}
+
+template <class T>
+void swap_buf(DevBuf<T>& a, DevBuf<T>& b) {
+    std::swap(a.p, b.p);
+    std::swap(a.cap, b.cap);
+}
+
+}  // namespace
+
+void DeviceTree::reserve_clusters(int n_needed, cudaStream_t s) {
+    if (n_needed <= cap) return;
+    const size_t c = size_t(n_needed) + n_needed / 2 + 64;
+    const size_t u = size_t(ncl);
+    face.grow_keep(c, u, s);
+    depth.grow_keep(c, u, s);
+    begin.grow_keep(c, u, s);
+    end.grow_keep(c, u, s);
+    parent.grow_keep(c, u, s);
+    nchild.grow_keep(c, u, s);
+    child.grow_keep(c, u, s);
+    xi0.grow_keep(c, u, s);
+    xi1.grow_keep(c, u, s);
+    eta0.grow_keep(c, u, s);
+    eta1.grow_keep(c, u, s);
+    cx.grow_keep(c, u, s);
+    cy.grow_keep(c, u, s);
+    cz.grow_keep(c, u, s);
+    rad.grow_keep(c, u, s);
+    split.grow_keep(c, u, s);
+    bnd.grow_keep(4 * c, 4 * u, s);
+    cap = int(c);
+}
+
+TreeView DeviceTree::view() const {
+    TreeView v;
+    v.n = n;
+    v.np = np;
+    v.npp = npp;
+    v.px = px;
+    v.py = py;
+    v.pz = pz;
+    v.xi = xi;
+    v.eta = eta;
+    v.w = has_w ? w.p : nullptr;
+    v.perm = perm;
+    v.node = node;
+    v.face = face;
+    v.depth = depth;
+    v.begin = begin;
+    v.end = end;
+    v.parent = parent;
+    v.nchild = nchild;
+    v.child = child;
+    v.xi0 = xi0;
+    v.xi1 = xi1;
+    v.eta0 = eta0;
+    v.eta1 = eta1;
+    v.cx = cx;
+    v.cy = cy;
+    v.cz = cz;
+    v.rad = rad;
+    v.qx = qx;
+    v.qy = qy;
+    v.qz = qz;
+    return v;
+}
+
+void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_in, long long n,
+                int degree, int n0, bool shrink, const Cheb& cheb, cudaStream_t s) {
+    t.n = n;
+    t.degree = degree;
+    t.np = degree + 1;
+    t.npp = t.np * t.np;
+    t.n0 = n0;
+    t.shrink = shrink;
+    t.has_w = w_in != nullptr;
+    t.ncl = 0;
+    t.level_first.clear();
+    t.level_count.clear();
+
+    for (DevBuf<double>* b : {&t.px, &t.py, &t.pz, &t.xi, &t.eta, &t.px2, &t.py2, &t.pz2, &t.xi2,
+                              &t.eta2, &sc.fxi, &sc.feta})
+        b->grow(n);
+    for (DevBuf<int>* b : {&t.perm, &t.node, &t.perm2, &t.node2, &t.rank, &sc.fface}) b->grow(n);
+    if (t.has_w) {
+        t.w.grow(n);
+        t.w2.grow(n);
+    }
+    sc.tiles.grow(scan_tile_ints(n, 6));
+    sc.grand.grow(8);
+    sc.counters.grow(8);
+    t.reserve_clusters(64, s);
+
+    const int gp = ceil_div(n, kThreads);
+
+    // ---- level 0: faces (cluster_tree.cpp:35-50) ------------------------------------------
+    k_face<<<gp, kThreads, 0, s>>>(xyz, n, sc.fface, sc.fxi, sc.feta);
+    CSFS_LAUNCH_CHECK();
+    {
+        const int* fface = sc.fface;
+        const double* fxi = sc.fxi;
+        const double* feta = sc.feta;
+        const int* grand = sc.grand;
+        double *px = t.px, *py = t.py, *pz = t.pz, *xi = t.xi, *eta = t.eta, *w = t.w;
+        int *perm = t.perm, *node = t.node;
+        const bool hw = t.has_w;
+        auto f = [=] __device__(long long i, int* c) { c[fface[i]] = 1; };
+        auto e = [=] __device__(long long i, const int* c, const int* pre) {
+            const int k = fface[i];
+            int base = 0;
+            for (int j = 0; j < k; ++j) base += grand[j];
+            const long long p = base + pre[k];
+            px[p] = xyz[3 * i];
+            py[p] = xyz[3 * i + 1];
+            pz[p] = xyz[3 * i + 2];
+            xi[p] = fxi[i];
+            eta[p] = feta[i];
+            perm[p] = int(i);
+            node[p] = k;
+            if (hw) w[p] = w_in[i];
+        };
+        run_scan<6>(n, f, e, sc.tiles, sc.grand, s);
+    }
+    k_roots<<<1, 32, 0, s>>>(cluster_ptrs(t), sc.grand);
+    CSFS_LAUNCH_CHECK();
+    t.ncl = 6;
+    t.level_first.push_back(0);
+    t.level_count.push_back(6);
+    finish_level(t, sc, 0, nullptr, 6, s);
+    CSFS_CK(cudaMemcpyAsync(sc.host, sc.counters.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaMemcpyAsync(sc.host + 2, sc.grand.p, 6 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaStreamSynchronize(s));
+    int nsplit = sc.host[1];
+    t.root_count.assign(sc.host + 2, sc.host + 8);
+
+    // ---- levels 1.. (cluster_tree.cpp:87-141) ----------------------------------------------
+    while (nsplit > 0) {
+        const int first = t.level_first.back();
+        const int cnt = t.level_count.back();
+        const int next_id = t.ncl;
+        t.reserve_clusters(t.ncl + 4 * nsplit, s);
+        sc.segP.grow(4 * size_t(cnt));
+        sc.segE.grow(4 * size_t(cnt));
+        sc.kid.grow(4 * size_t(cnt));
+        sc.koff.grow(4 * size_t(cnt));
+        ClusterPtrs c = cluster_ptrs(t);
+        {
+            const int* node = t.node;
+            const double* xi = t.xi;
+            const double* eta = t.eta;
+            int* rank = t.rank;
+            int* segP = sc.segP;
+            int* segE = sc.segE;
+            auto f = [=] __device__(long long i, int* cc) {
+                const int nd = node[i];
+                if (nd >= first && nd < first + cnt && c.split[nd])
+                    cc[quadrant_of(c, nd, xi[i], eta[i])] = 1;
+            };
+            auto e = [=] __device__(long long i, const int* cc, const int* pre) {
+                const int nd = node[i];
+                if (!(nd >= first && nd < first + cnt && c.split[nd])) return;
+                const int q = cc[0] ? 0 : cc[1] ? 1 : cc[2] ? 2 : 3;
+                rank[i] = pre[q];
+                const int fi = nd - first;
+                if (i == c.begin[nd])
+                    for (int k = 0; k < 4; ++k) segP[4 * fi + k] = pre[k];
+                if (i == c.end[nd] - 1)
+                    for (int k = 0; k < 4; ++k) segE[4 * fi + k] = pre[k] + cc[k];
+            };
+            run_scan<4>(n, f, e, sc.tiles, sc.grand, s);
+        }
+        k_children<<<1, kScanThreads, 0, s>>>(first, cnt, next_id, c, sc.segP, sc.segE, sc.kid,
+                                               sc.koff, sc.counters.p);
+        CSFS_LAUNCH_CHECK();
+        PartArrays a{t.px,  t.py,  t.pz,  t.xi,    t.eta,   t.has_w ? t.w.p : nullptr,
+                     t.perm, t.node, t.px2, t.py2, t.pz2,   t.xi2,
+                     t.eta2, t.has_w ? t.w2.p : nullptr, t.perm2, t.node2};
+        k_scatter<<<gp, kThreads, 0, s>>>(n, first, cnt, c, a, t.rank, sc.segP, sc.kid, sc.koff);
+        CSFS_LAUNCH_CHECK();
+        swap_buf(t.px, t.px2);
+        swap_buf(t.py, t.py2);
+        swap_buf(t.pz, t.pz2);
+        swap_buf(t.xi, t.xi2);
+        swap_buf(t.eta, t.eta2);
+        swap_buf(t.perm, t.perm2);
+        swap_buf(t.node, t.node2);
+        if (t.has_w) swap_buf(t.w, t.w2);
+
+        finish_level(t, sc, next_id, sc.counters.p, 4 * nsplit, s);
+        CSFS_CK(cudaMemcpyAsync(sc.host, sc.counters.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
+        const int nnew = sc.host[0];
+        nsplit = sc.host[1];
+        t.ncl += nnew;
+        t.level_first.push_back(next_id);
+        t.level_count.push_back(nnew);
+    }
+
+    // ---- proxy points --------------------------------------------------------------------
+    const long long nq = (long long)t.ncl * t.npp;
+    t.qx.grow(nq);
+    t.qy.grow(nq);
+    t.qz.grow(nq);
+    k_proxy<<<ceil_div(nq, kThreads), kThreads, 0, s>>>(t.ncl, t.np, cheb, t.face, t.xi0, t.xi1,
+                                                          t.eta0, t.eta1, t.qx, t.qy, t.qz);
+    CSFS_LAUNCH_CHECK();
+}
+
+bool device_equal(const void* a, const void* b, size_t bytes, Scratch& sc, cudaStream_t s) {
+    if (a == b) return true;
+    sc.counters.grow(8);
+    CSFS_CK(cudaMemsetAsync(sc.counters.p + 4, 0, sizeof(int), s));
+    const long long n = (long long)(bytes / 8);
+    k_equal<<<592, 256, 0, s>>>(static_cast<const unsigned long long*>(a),
+                                 static_cast<const unsigned long long*>(b), n, sc.counters.p + 4);
+    CSFS_LAUNCH_CHECK();
+    CSFS_CK(cudaMemcpyAsync(sc.host + 4, sc.counters.p + 4, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaStreamSynchronize(s));
+    return sc.host[4] == 0;
+}
+
+// LIFO expansion order of the reference (cluster_tree.cpp:87-140): the stack starts as
+// roots 0..5 (5 on top); popping a node that splits appends its children (ids =
+// clusters.size() in quadrant order) and pushes them, so the last child is expanded next.
+// Replaying that order over the GPU topology reproduces the reference ids exactly.
+std::vector<int> reference_ids(const std::vector<int>& parent, const std::vector<int>& depth,
+                               const std::vector<int4>& child, const std::vector<int>& nchild) {
+    (void)parent;
+    (void)depth;
+    const int ncl = int(nchild.size());
+    std::vector<int> ref(ncl, -1);
+    for (int r = 0; r < 6 && r < ncl; ++r) ref[r] = r;
+    int next = 6;
+    std::vector<int> stack = {0, 1, 2, 3, 4, 5};
+    while (!stack.empty()) {
+        const int id = stack.back();
+        stack.pop_back();
+        const int4 ch = child[id];
+        const int cs[4] = {ch.x, ch.y, ch.z, ch.w};
+        for (int q = 0; q < nchild[id]; ++q) {
+            ref[cs[q]] = next++;
+            stack.push_back(cs[q]);
+        }
+    }
+    return ref;
+}
+
+}  // namespace csfs_b200

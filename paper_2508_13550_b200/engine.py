@@ -1,0 +1,301 @@
+"""Python binding of the C-ABI (include/csfs_b200.h) — used by the tests and bench.py.
+
+It mirrors the reference's C++ summation API (/root/reference/proj/include/csfs/
+summation.hpp, kernels.hpp): ``Kernel`` / ``SalParams`` / ``TraversalConfig`` /
+``SumStats`` / ``PotentialField`` and ``csfmm_sum`` / ``direct_sum`` /
+``summed_potential``, with the same argument meaning and the same
+``ValueError``-for-``std::invalid_argument`` behaviour and messages.  Every call goes
+through libcsfs_b200.so; there is no CPU path — if the library or an sm_100 device is
+missing, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcsfs_b200.so")
+
+OK, INVALID_ARGUMENT, CUDA_ERROR, NCCL_ERROR, OUT_OF_MEMORY = 0, 1, 2, 3, 4
+
+
+class KernelKind(enum.IntEnum):
+    Laplace = 0
+    Biharmonic = 1
+    BiotSavart = 2
+    Sal = 3
+
+
+class Method(enum.IntEnum):
+    Direct = 0
+    Cstc = 1
+    Csfmm = 2
+
+
+_KIND_NAMES = {"laplace": KernelKind.Laplace, "biharmonic": KernelKind.Biharmonic,
+               "biot_savart": KernelKind.BiotSavart, "sal": KernelKind.Sal}
+
+
+@dataclass
+class SalParams:  # kernels.hpp:18-23
+    a1: float = -2.7
+    b0: float = -6.21196
+    b1: float = 6.1
+    rho_ratio: float = 1025.0 / 5517.0
+
+
+@dataclass
+class Kernel:  # kernels.hpp:32-49
+    kind: KernelKind = KernelKind.Laplace
+    sal: SalParams = field(default_factory=SalParams)
+
+    def out_dim(self) -> int:
+        return 3 if self.kind == KernelKind.BiotSavart else 1
+
+    def singular_at_coincidence(self) -> bool:
+        return self.kind != KernelKind.Biharmonic
+
+    def name(self) -> str:
+        return {v: k for k, v in _KIND_NAMES.items()}[KernelKind(self.kind)]
+
+    @staticmethod
+    def parse(name: str, sal: SalParams | None = None) -> "Kernel":
+        if name not in _KIND_NAMES:
+            raise ValueError("unknown kernel: " + name)
+        return Kernel(_KIND_NAMES[name], sal or SalParams())
+
+
+@dataclass
+class TraversalConfig:  # summation.hpp:22-31
+    method: Method = Method.Csfmm
+    mac: float = 0.7
+    degree: int = 6
+    n0: int = -1
+    shrink: bool = True
+    threads: int = 0  # accepted for API parity; the device decides its own parallelism
+
+    def resolved_n0(self) -> int:
+        return self.n0 if self.n0 >= 0 else 4 * self.degree * self.degree
+
+
+class _CKernel(C.Structure):
+    _fields_ = [("kind", C.c_int), ("a1", C.c_double), ("b0", C.c_double), ("b1", C.c_double),
+                ("rho_ratio", C.c_double)]
+
+
+class _CConfig(C.Structure):
+    _fields_ = [("mac", C.c_double), ("degree", C.c_int), ("n0", C.c_int), ("shrink", C.c_int)]
+
+
+class SumStats(C.Structure):  # summation.hpp:44-53 + B200 extras
+    _fields_ = [("t_tree_build", C.c_double), ("t_upward", C.c_double), ("t_traversal", C.c_double),
+                ("t_downward", C.c_double), ("t_total", C.c_double),
+                ("pp", C.c_uint64), ("pc", C.c_uint64), ("cp", C.c_uint64), ("cc", C.c_uint64),
+                ("src_depth", C.c_int), ("src_clusters", C.c_int), ("src_leaves", C.c_int),
+                ("tgt_depth", C.c_int), ("tgt_clusters", C.c_int), ("tgt_leaves", C.c_int),
+                ("t_lists", C.c_double), ("t_interact", C.c_double),
+                ("evals_pp", C.c_uint64), ("evals_pc", C.c_uint64), ("evals_cp", C.c_uint64),
+                ("evals_cc", C.c_uint64), ("shared_tree", C.c_int)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+@dataclass
+class PotentialField:  # summation.hpp:34-41
+    out_dim: int
+    values: np.ndarray  # (n * out_dim,) target-major, input order
+
+    def size(self) -> int:
+        return self.values.size // self.out_dim
+
+
+@dataclass
+class ParticleSet:  # cluster_tree.hpp:13-18
+    positions: np.ndarray  # (n, 3)
+    weights: np.ndarray  # (n,)
+
+    def size(self) -> int:
+        return self.positions.shape[0]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libcsfs_b200.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P, S, I, D = C.c_void_p, C.c_size_t, C.c_int, C.POINTER(C.c_double)
+        L.csfs_b200_create.argtypes = [C.POINTER(P), I]
+        L.csfs_b200_destroy.argtypes = [P]
+        L.csfs_b200_last_error.argtypes = [P]
+        L.csfs_b200_last_error.restype = C.c_char_p
+        L.csfs_b200_csfmm.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), C.POINTER(_CConfig), P,
+                                      C.POINTER(SumStats)]
+        L.csfs_b200_csfmm_device.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), C.POINTER(_CConfig),
+                                             P, C.POINTER(SumStats), P]
+        L.csfs_b200_direct.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), P]
+        L.csfs_b200_direct_device.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), P, P]
+        L.csfs_b200_tree_info.argtypes = [P, I, C.POINTER(I), C.POINTER(I), C.POINTER(S), C.POINTER(I)]
+        L.csfs_b200_tree_export.argtypes = [P, I, P, P, P, P]
+        L.csfs_b200_lists_export.argtypes = [P, C.POINTER(C.c_longlong), P, P, P, P]
+        L.csfs_b200_proxy_weights_export.argtypes = [P, P]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+def _ckernel(k: Kernel) -> _CKernel:
+    return _CKernel(int(k.kind), k.sal.a1, k.sal.b0, k.sal.b1, k.sal.rho_ratio)
+
+
+def _cconfig(c: TraversalConfig) -> _CConfig:
+    return _CConfig(float(c.mac), int(c.degree), int(c.n0), 1 if c.shrink else 0)
+
+
+class Engine:
+    """One csfs_b200_ctx: one device, one stream, reusable device buffers."""
+
+    def __init__(self, device: int = 0):
+        self._lib = lib()
+        h = C.c_void_p()
+        rc = self._lib.csfs_b200_create(C.byref(h), int(device))
+        if rc != OK:
+            raise RuntimeError(f"csfs_b200_create(device={device}) failed with code {rc} "
+                               "(needs an sm_100 GPU; there is no CPU fallback)")
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.csfs_b200_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc == OK:
+            return
+        msg = self._lib.csfs_b200_last_error(self._h).decode()
+        if rc == INVALID_ARGUMENT:
+            raise ValueError(msg)
+        if rc == OUT_OF_MEMORY:
+            raise MemoryError(msg)
+        raise RuntimeError(f"csfs_b200 error {rc}: {msg}")
+
+    # --- reference API mirror --------------------------------------------------------
+    def csfmm_sum(self, targets: ParticleSet, sources: ParticleSet, kernel: Kernel,
+                  config: TraversalConfig, stats: SumStats | None = None) -> PotentialField:
+        tx = np.ascontiguousarray(targets.positions, dtype=np.float64)
+        sx = tx if sources.positions is targets.positions else np.ascontiguousarray(sources.positions, dtype=np.float64)
+        sw = np.ascontiguousarray(sources.weights, dtype=np.float64)
+        if sw.shape[0] != sx.shape[0]:
+            raise ValueError("weight count does not match particle count")
+        out = np.empty(tx.shape[0] * kernel.out_dim())
+        st = stats if stats is not None else SumStats()
+        self._check(self._lib.csfs_b200_csfmm(self._h, _ptr(tx), tx.shape[0], _ptr(sx), _ptr(sw), sx.shape[0],
+                                              C.byref(_ckernel(kernel)), C.byref(_cconfig(config)), _ptr(out),
+                                              C.byref(st)))
+        return PotentialField(kernel.out_dim(), out)
+
+    def direct_sum(self, targets: ParticleSet, sources: ParticleSet, kernel: Kernel,
+                   threads: int = 0) -> PotentialField:
+        tx = np.ascontiguousarray(targets.positions, dtype=np.float64)
+        sx = np.ascontiguousarray(sources.positions, dtype=np.float64)
+        sw = np.ascontiguousarray(sources.weights, dtype=np.float64)
+        if sw.shape[0] != sx.shape[0]:
+            raise ValueError("source weights and positions differ in length")
+        out = np.empty(tx.shape[0] * kernel.out_dim())
+        self._check(self._lib.csfs_b200_direct(self._h, _ptr(tx), tx.shape[0], _ptr(sx), _ptr(sw), sx.shape[0],
+                                               C.byref(_ckernel(kernel)), _ptr(out)))
+        return PotentialField(kernel.out_dim(), out)
+
+    def summed_potential(self, targets, sources, kernel, config, stats=None) -> PotentialField:
+        if config.method == Method.Direct:
+            return self.direct_sum(targets, sources, kernel)
+        if config.method == Method.Cstc:
+            raise NotImplementedError("CSTC (summation.cpp:308-381) is not on the B200 hot path yet")
+        return self.csfmm_sum(targets, sources, kernel, config, stats)
+
+    # --- device-resident entry (torch tensors / raw device pointers) --------------------
+    def csfmm_device(self, tgt_xyz_ptr: int, nt: int, src_xyz_ptr: int, src_w_ptr: int, ns: int,
+                     kernel: Kernel, config: TraversalConfig, out_ptr: int, stream: int = 0,
+                     stats: SumStats | None = None) -> SumStats:
+        st = stats if stats is not None else SumStats()
+        self._check(self._lib.csfs_b200_csfmm_device(
+            self._h, C.c_void_p(tgt_xyz_ptr), nt, C.c_void_p(src_xyz_ptr), C.c_void_p(src_w_ptr), ns,
+            C.byref(_ckernel(kernel)), C.byref(_cconfig(config)), C.c_void_p(out_ptr), C.byref(st),
+            C.c_void_p(stream)))
+        return st
+
+    def direct_device(self, tgt_xyz_ptr, nt, src_xyz_ptr, src_w_ptr, ns, kernel, out_ptr, stream=0):
+        self._check(self._lib.csfs_b200_direct_device(
+            self._h, C.c_void_p(tgt_xyz_ptr), nt, C.c_void_p(src_xyz_ptr), C.c_void_p(src_w_ptr), ns,
+            C.byref(_ckernel(kernel)), C.c_void_p(out_ptr), C.c_void_p(stream)))
+
+    # --- stepwise exports of the last csfmm call ------------------------------------------
+    def tree_info(self, which: int) -> tuple[int, int, int, int]:
+        ncl, depth, npp = C.c_int(), C.c_int(), C.c_int()
+        n = C.c_size_t()
+        self._check(self._lib.csfs_b200_tree_info(self._h, which, C.byref(ncl), C.byref(depth), C.byref(n),
+                                                  C.byref(npp)))
+        return ncl.value, depth.value, n.value, npp.value
+
+    def tree_export(self, which: int) -> dict:
+        ncl, depth, n, npp = self.tree_info(which)
+        perm = np.empty(n, np.int32)
+        ints = np.empty((ncl, 10), np.int32)
+        dbls = np.empty((ncl, 8))
+        proxy = np.empty((ncl, npp, 3))
+        self._check(self._lib.csfs_b200_tree_export(self._h, which, _ptr(perm), _ptr(ints), _ptr(dbls), _ptr(proxy)))
+        return {"perm": perm, "ints": ints, "dbls": dbls, "proxy": proxy, "depth": depth}
+
+    def lists_export(self) -> dict:
+        counts = (C.c_longlong * 4)()
+        self._check(self._lib.csfs_b200_lists_export(self._h, counts, None, None, None, None))
+        bufs = [np.empty((max(counts[k], 0), 2), np.int32) for k in range(4)]
+        self._check(self._lib.csfs_b200_lists_export(self._h, counts, *[_ptr(b) for b in bufs]))
+        return dict(zip(["pp", "pc", "cp", "cc"], bufs))
+
+    def proxy_weights_export(self) -> np.ndarray:
+        ncl, _, _, npp = self.tree_info(1)
+        pw = np.empty((ncl, npp))
+        self._check(self._lib.csfs_b200_proxy_weights_export(self._h, _ptr(pw)))
+        return pw
+
+
+_default: Engine | None = None
+
+
+def default_engine() -> Engine:
+    global _default
+    if _default is None:
+        _default = Engine(0)
+    return _default
+
+
+def csfmm_sum(targets, sources, kernel, config, stats=None) -> PotentialField:
+    return default_engine().csfmm_sum(targets, sources, kernel, config, stats)
+
+
+def direct_sum(targets, sources, kernel, threads=0) -> PotentialField:
+    return default_engine().direct_sum(targets, sources, kernel, threads)
+
+
+def summed_potential(targets, sources, kernel, config, stats=None) -> PotentialField:
+    return default_engine().summed_potential(targets, sources, kernel, config, stats)
