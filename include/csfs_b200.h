@@ -24,6 +24,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define CSFS_B200_API __attribute__((visibility("default")))
+#else
+#define CSFS_B200_API
+#endif
+
 #define CSFS_B200_OK 0
 #define CSFS_B200_INVALID_ARGUMENT 1
 #define CSFS_B200_CUDA_ERROR 2
@@ -63,49 +69,87 @@ typedef struct {
 } csfs_b200_stats;
 
 /* --- lifetime ------------------------------------------------------------------------ */
-int csfs_b200_create(csfs_b200_ctx** out, int device);
-void csfs_b200_destroy(csfs_b200_ctx* ctx);
+CSFS_B200_API int csfs_b200_create(csfs_b200_ctx** out, int device);
+CSFS_B200_API void csfs_b200_destroy(csfs_b200_ctx* ctx);
 /* Message of the last failing call on this context ("" if none). */
-const char* csfs_b200_last_error(const csfs_b200_ctx* ctx);
+CSFS_B200_API const char* csfs_b200_last_error(const csfs_b200_ctx* ctx);
 
 /* --- the hot path ---------------------------------------------------------------------
  * csfs::csfmm_sum (summation.hpp:81-83, summation.cpp:383-421).  HOST pointers:
  * tgt_xyz nt x 3, src_xyz ns x 3, src_w ns, out nt x out_dim (overwritten).
  * stats may be NULL.  Synchronous. */
-int csfs_b200_csfmm(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt, const double* src_xyz,
+CSFS_B200_API int csfs_b200_csfmm(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt, const double* src_xyz,
                     const double* src_w, size_t ns, const csfs_b200_kernel* kernel,
                     const csfs_b200_config* config, double* out, csfs_b200_stats* stats);
 
 /* Same, DEVICE pointers (on the context's device), work ordered on `stream`
- * (cudaStream_t, NULL = the context's own stream).  Returns after the result is in
+ * (cudaStream_t; NULL = CUDA's legacy default stream).  Returns after the result is in
  * `out` (the engine synchronizes on tree/list sizes). */
-int csfs_b200_csfmm_device(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt,
+CSFS_B200_API int csfs_b200_csfmm_device(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt,
                            const double* src_xyz, const double* src_w, size_t ns,
                            const csfs_b200_kernel* kernel, const csfs_b200_config* config,
                            double* out, csfs_b200_stats* stats, void* stream);
 
 /* csfs::direct_sum (summation.hpp:74-75, summation.cpp:136-161): O(nt*ns) all pairs. */
-int csfs_b200_direct(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt, const double* src_xyz,
+CSFS_B200_API int csfs_b200_direct(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt, const double* src_xyz,
                      const double* src_w, size_t ns, const csfs_b200_kernel* kernel, double* out);
-int csfs_b200_direct_device(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt,
+CSFS_B200_API int csfs_b200_direct_device(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt,
                             const double* src_xyz, const double* src_w, size_t ns,
                             const csfs_b200_kernel* kernel, double* out, void* stream);
 
 /* --- stepwise state of the LAST csfmm call (parity / inspection) ------------------------
  * which: 0 target tree, 1 source tree.  Cluster ids are the REFERENCE's ids
  * (LIFO expansion order, cluster_tree.cpp:87-140). */
-int csfs_b200_tree_info(const csfs_b200_ctx* ctx, int which, int* n_clusters, int* depth,
+CSFS_B200_API int csfs_b200_tree_info(const csfs_b200_ctx* ctx, int which, int* n_clusters, int* depth,
                         size_t* n_particles, int* n_proxy_per_cluster);
 /* perm: n (tree order -> input index); ints: ncl x 10 = face, begin, end, parent, depth,
  * child_count, children[4]; dbls: ncl x 8 = xi0, xi1, eta0, eta1, cx, cy, cz, radius;
  * proxy: ncl x (p+1)^2 x 3.  Any pointer may be NULL. */
-int csfs_b200_tree_export(csfs_b200_ctx* ctx, int which, int* perm, int* ints, double* dbls,
+CSFS_B200_API int csfs_b200_tree_export(csfs_b200_ctx* ctx, int which, int* perm, int* ints, double* dbls,
                           double* proxy);
 /* counts[4] = |pp|,|pc|,|cp|,|cc|; lists as (t, s) int pairs in reference ids, sorted. */
-int csfs_b200_lists_export(csfs_b200_ctx* ctx, long long* counts, int* pp, int* pc, int* cp,
+CSFS_B200_API int csfs_b200_lists_export(csfs_b200_ctx* ctx, long long* counts, int* pp, int* pc, int* cp,
                            int* cc);
 /* Source-tree proxy weights after the upward pass, ncl x (p+1)^2, reference id order. */
-int csfs_b200_proxy_weights_export(csfs_b200_ctx* ctx, double* pw);
+CSFS_B200_API int csfs_b200_proxy_weights_export(csfs_b200_ctx* ctx, double* pw);
+
+/* --- multi-GPU: target partitioning, one process per GPU ----------------------------------
+ * The library is collective-agnostic: the CALLER owns two device buffers (sizes from
+ * part_sizes) and all-reduces (sum) them between the phases (torch.distributed / NCCL
+ * over NVLink in paper_2508_13550_b200/distributed.py).  Every rank, on `stream`:
+ *   1. part_plan     full trees, dual traversal and work items (redundant, cheap);
+ *   2. part_units    the partition units (depth-1 subtrees + unsplit roots, tree order)
+ *                    with particle ranges and cost; the caller splits them into one
+ *                    contiguous particle range per rank (targets: by cost, sources: count);
+ *   3. part_upward   writes the owned source subtrees' proxy weights into pw, zeros
+ *                    elsewhere              -> caller: all_reduce(sum, pw)
+ *   4. part_eval     takes the reduced pw, computes the depth-0 proxy weights
+ *                    (redundantly), the owned targets' PP/PC/CP/CC and downward pass into
+ *                    the TREE-ORDER field phi, zeros elsewhere
+ *                                           -> caller: all_reduce(sum, phi)
+ *   5. part_finish   out[perm[t]] = phi_reduced[t] (device out, input order).
+ * Each target is evaluated by exactly one rank in the single-GPU order and every reduced
+ * slot has one non-zero term, so the result is bitwise identical to
+ * csfs_b200_csfmm_device for any rank count. */
+CSFS_B200_API int csfs_b200_part_plan(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt,
+                                      const double* src_xyz, const double* src_w, size_t ns,
+                                      const csfs_b200_kernel* kernel,
+                                      const csfs_b200_config* config, void* stream);
+CSFS_B200_API int csfs_b200_part_units(csfs_b200_ctx* ctx, int which, int* n_units,
+                                       long long* begin, long long* end, double* cost);
+CSFS_B200_API int csfs_b200_part_sizes(csfs_b200_ctx* ctx, size_t* n_pw, size_t* n_phi);
+CSFS_B200_API int csfs_b200_part_upward(csfs_b200_ctx* ctx, long long src_begin,
+                                        long long src_end, double* pw);
+CSFS_B200_API int csfs_b200_part_eval(csfs_b200_ctx* ctx, long long tgt_begin, long long tgt_end,
+                                      const double* pw_reduced, double* phi);
+CSFS_B200_API int csfs_b200_part_finish(csfs_b200_ctx* ctx, const double* phi_reduced,
+                                        double* out);
+
+/* --- diagnostics ------------------------------------------------------------------------ */
+/* Number of engine kernels launched by this process so far (all contexts). */
+CSFS_B200_API uint64_t csfs_b200_kernel_launches(void);
+/* Measured FP64 FMA-pipe peak of the context's device in TFLOP/s (DFMA = 2 flops). */
+CSFS_B200_API int csfs_b200_probe_fp64(csfs_b200_ctx* ctx, double* tflops);
 
 #ifdef __cplusplus
 }

@@ -37,7 +37,12 @@ struct csfs_b200_ctx {
     FmmConfig cfg;
     bool have_state = false;
     int dim = 1;
-    int n_internal_t = 0, n_internal_s = 0;
+    // multi-GPU partition state (csfs_b200_part_*)
+    bool part_planned = false;
+    cudaStream_t part_stream = nullptr;
+    DevBuf<double> phi_tree;
+    std::vector<long long> unit_b[2], unit_e[2];
+    std::vector<double> unit_cost[2];
 };
 
 namespace {
@@ -161,10 +166,10 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     CSFS_CK(cudaMemsetAsync(c->phi_near.p, 0, nt * dim * sizeof(double), s));
     CSFS_CK(cudaMemsetAsync(T.qphi.p, 0, size_t(T.ncl) * T.npp * dim * sizeof(double), s));
     c->counter.grow(4);
-    interact(ks, T, S, c->items, c->phi_near, c->counter, s);
+    interact(ks, T, S, c->items, c->phi_near, c->counter, s, Own{0, (long long)nt});
     CSFS_CK(cudaEventRecord(ev[4], s));
 
-    downward_pass(T, c->cheb, dim, c->phi_near, out, s);
+    downward_pass(T, c->cheb, dim, c->phi_near, out, s, Own{0, (long long)nt}, true);
     CSFS_CK(cudaEventRecord(ev[5], s));
     CSFS_CK(cudaEventSynchronize(ev[5]));
     c->have_state = true;
@@ -196,9 +201,10 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     }
 }
 
-cudaStream_t pick(csfs_b200_ctx* c, void* stream) {
-    return stream ? static_cast<cudaStream_t>(stream) : c->own;
-}
+// Device-pointer entry points run on the caller's stream; NULL is CUDA's legacy default
+// stream (what torch reports as cuda_stream == 0), never a private stream, so work stays
+// ordered with the caller's producers and consumers.
+cudaStream_t pick(csfs_b200_ctx*, void* stream) { return static_cast<cudaStream_t>(stream); }
 
 struct HostTree {
     std::vector<int> face, depth, begin, end, parent, nchild, ref, inv;
@@ -433,6 +439,145 @@ int csfs_b200_proxy_weights_export(csfs_b200_ctx* c, double* pw) {
         for (int i = 0; i < s.ncl; ++i)
             std::memcpy(pw + size_t(h.ref[i]) * s.npp, q.data() + size_t(i) * s.npp, s.npp * sizeof(double));
     });
+}
+
+// --- multi-GPU target partitioning ------------------------------------------------------
+
+int csfs_b200_part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
+                        const double* sw, size_t ns, const csfs_b200_kernel* k,
+                        const csfs_b200_config* cfg, void* stream) {
+    return guarded(c, [&] {
+        const KernelSpec ks = to_spec(k);
+        const FmmConfig f = to_cfg(cfg);
+        validate(f, nt, ns);
+        cudaStream_t s = pick(c, stream);
+        c->have_state = false;
+        c->part_planned = false;
+        c->part_stream = s;
+        c->kspec = ks;
+        c->cfg = f;
+        c->dim = ks.out_dim();
+        c->cheb = make_cheb(f.degree);
+        const int n0 = f.resolved_n0();
+        c->shared = (nt == ns) && device_equal(txyz, sxyz, nt * 3 * sizeof(double), c->sc, s);
+        DeviceTree& T = c->ttree;
+        DeviceTree& S = c->shared ? c->ttree : c->stree;
+        build_tree(T, c->sc, txyz, c->shared ? sw : nullptr, (long long)nt, f.degree, n0, f.shrink, c->cheb, s);
+        if (!c->shared) build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s);
+        dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
+        build_items(T, S, c->lists, c->items, c->sc, s);
+        // partition units: depth-1 subtrees plus unsplit roots, in tree order
+        for (int w = 0; w < 2; ++w) {
+            const DeviceTree& t = (w == 0 || c->shared) ? T : S;
+            const int nfirst = t.depth_max() >= 1 ? t.level_first[1] + t.level_count[1] : 6;
+            std::vector<int> b(nfirst), e(nfirst), nch(nfirst), dep(nfirst);
+            CSFS_CK(cudaMemcpy(b.data(), t.begin.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
+            CSFS_CK(cudaMemcpy(e.data(), t.end.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
+            CSFS_CK(cudaMemcpy(nch.data(), t.nchild.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
+            CSFS_CK(cudaMemcpy(dep.data(), t.depth.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
+            std::vector<std::pair<long long, long long>> u;
+            for (int i = 0; i < nfirst; ++i)
+                if (e[i] > b[i] && (dep[i] == 1 || nch[i] == 0)) u.push_back({b[i], e[i]});
+            std::sort(u.begin(), u.end());
+            c->unit_b[w].clear();
+            c->unit_e[w].clear();
+            for (auto& p : u) {
+                c->unit_b[w].push_back(p.first);
+                c->unit_e[w].push_back(p.second);
+            }
+            c->unit_cost[w].assign(u.size(), 0.0);
+            if (w == 1)
+                for (size_t i = 0; i < u.size(); ++i) c->unit_cost[1][i] = double(u[i].second - u[i].first);
+        }
+        {
+            const int ni = c->items.n_items;
+            std::vector<int> anchor(ni);
+            std::vector<double> cost(ni);
+            if (ni) {
+                CSFS_CK(cudaMemcpy(anchor.data(), c->items.anchor.p, ni * sizeof(int), cudaMemcpyDeviceToHost));
+                CSFS_CK(cudaMemcpy(cost.data(), c->items.cost.p, ni * sizeof(double), cudaMemcpyDeviceToHost));
+            }
+            const auto& ub = c->unit_b[0];
+            for (int i = 0; i < ni; ++i) {
+                if (anchor[i] < 0) continue;
+                const size_t u = size_t(std::upper_bound(ub.begin(), ub.end(), (long long)anchor[i]) - ub.begin()) - 1;
+                c->unit_cost[0][u] += cost[i];
+            }
+        }
+        c->part_planned = true;
+    });
+}
+
+int csfs_b200_part_units(csfs_b200_ctx* c, int which, int* n_units, long long* begin, long long* end,
+                         double* cost) {
+    return guarded(c, [&] {
+        if (!c->part_planned) throw InvalidArgument("call csfs_b200_part_plan first");
+        if (which != 0 && which != 1) throw InvalidArgument("which must be 0 (target) or 1 (source)");
+        const size_t n = c->unit_b[which].size();
+        if (n_units) *n_units = int(n);
+        for (size_t i = 0; i < n; ++i) {
+            if (begin) begin[i] = c->unit_b[which][i];
+            if (end) end[i] = c->unit_e[which][i];
+            if (cost) cost[i] = c->unit_cost[which][i];
+        }
+    });
+}
+
+int csfs_b200_part_sizes(csfs_b200_ctx* c, size_t* n_pw, size_t* n_phi) {
+    return guarded(c, [&] {
+        if (!c->part_planned) throw InvalidArgument("call csfs_b200_part_plan first");
+        const DeviceTree& S = c->shared ? c->ttree : c->stree;
+        if (n_pw) *n_pw = size_t(S.ncl) * S.npp;
+        if (n_phi) *n_phi = size_t(c->ttree.n) * c->dim;
+    });
+}
+
+int csfs_b200_part_upward(csfs_b200_ctx* c, long long src_b, long long src_e, double* pw) {
+    return guarded(c, [&] {
+        if (!c->part_planned) throw InvalidArgument("call csfs_b200_part_plan first");
+        DeviceTree& S = c->shared ? c->ttree : c->stree;
+        upward_pass(S, c->cheb, c->part_stream, 1, Own{src_b, src_e});
+        CSFS_CK(cudaMemcpyAsync(pw, S.qw.p, size_t(S.ncl) * S.npp * sizeof(double), cudaMemcpyDeviceToDevice,
+                                c->part_stream));
+    });
+}
+
+int csfs_b200_part_eval(csfs_b200_ctx* c, long long tgt_b, long long tgt_e, const double* pw_reduced,
+                        double* phi) {
+    return guarded(c, [&] {
+        if (!c->part_planned) throw InvalidArgument("call csfs_b200_part_plan first");
+        cudaStream_t s = c->part_stream;
+        DeviceTree& T = c->ttree;
+        DeviceTree& S = c->shared ? c->ttree : c->stree;
+        CSFS_CK(cudaMemcpyAsync(S.qw.p, pw_reduced, size_t(S.ncl) * S.npp * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+        upward_pass(S, c->cheb, s, 2);  // depth-0 proxy weights, from the reduced depth-1 ones
+        const int dim = c->dim;
+        const size_t nt = size_t(T.n);
+        c->phi_near.grow(nt * dim);
+        T.qphi.grow(size_t(T.ncl) * T.npp * dim);
+        CSFS_CK(cudaMemsetAsync(c->phi_near.p, 0, nt * dim * sizeof(double), s));
+        CSFS_CK(cudaMemsetAsync(phi, 0, nt * dim * sizeof(double), s));
+        CSFS_CK(cudaMemsetAsync(T.qphi.p, 0, size_t(T.ncl) * T.npp * dim * sizeof(double), s));
+        c->counter.grow(4);
+        interact(c->kspec, T, S, c->items, c->phi_near, c->counter, s, Own{tgt_b, tgt_e});
+        downward_pass(T, c->cheb, dim, c->phi_near, phi, s, Own{tgt_b, tgt_e}, false);
+    });
+}
+
+int csfs_b200_part_finish(csfs_b200_ctx* c, const double* phi_reduced, double* out) {
+    return guarded(c, [&] {
+        if (!c->part_planned) throw InvalidArgument("call csfs_b200_part_plan first");
+        scatter_to_input(c->ttree, c->dim, phi_reduced, out, c->part_stream);
+        CSFS_CK(cudaStreamSynchronize(c->part_stream));
+        c->have_state = true;
+    });
+}
+
+uint64_t csfs_b200_kernel_launches(void) { return launch_counter(); }
+
+int csfs_b200_probe_fp64(csfs_b200_ctx* c, double* tflops) {
+    return guarded(c, [&] { *tflops = probe_fp64_tflops(c->own); });
 }
 
 }  // extern "C"

@@ -43,7 +43,14 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     throw CudaFailure(msg);
 }
 #define CSFS_CK(x) ::csfs_b200::cuda_check((x), #x, __FILE__, __LINE__)
-#define CSFS_LAUNCH_CHECK() ::csfs_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+// Every kernel launch of the engine goes through this check; it also counts launches so
+// bench.py can report how many of OUR kernels ran in its timed region.
+unsigned long long& launch_counter();
+#define CSFS_LAUNCH_CHECK()                                                                  \
+    do {                                                                                     \
+        ++::csfs_b200::launch_counter();                                                     \
+        ::csfs_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);   \
+    } while (0)
 
 // Second-kind Chebyshev grid (interpolation.cpp:14-24), passed by value into kernels.
 // Nodes/weights are computed on the host with the same libm call the reference makes

@@ -120,6 +120,8 @@ struct Items {
     DevBuf<long long> code;     // per entry sort code
     DevBuf<int2> seg;           // per entry source segment
     DevBuf<int4> item;          // {tgt_start, tgt_len (neg = proxy), seg_begin, seg_end}
+    DevBuf<int> anchor;         // owner key: first target particle, -1 = every rank
+    DevBuf<double> cost;        // pair evaluations of the item
     DevBuf<unsigned long long> pairs;  // 4 pair-eval counters (pp, pc, cp, cc)
     int n_items = 0;
     long long n_entries = 0;
@@ -153,9 +155,17 @@ void build_tree(DeviceTree& tree, Scratch& sc, const double* xyz, const double* 
 bool device_equal(const void* a, const void* b, size_t bytes, Scratch& sc, cudaStream_t s);
 
 // passes.cu
-void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s);
+// Ownership window of one rank: clusters at depth >= 1 whose first particle lies in
+// [b, e) (tree order).  The whole range is [0, n).
+struct Own {
+    long long b = 0, e = 0;
+};
+// mode: 0 all clusters; 1 owned clusters at depth >= 1 only (qw zeroed elsewhere);
+//       2 depth-0 clusters only (after the proxy-weight allreduce)
+void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s, int mode = 0, Own own = {});
+// out_perm = true: out[perm[t]] (input order); false: out[t] (tree order, owned leaves only).
 void downward_pass(DeviceTree& tgt, const Cheb& cheb, int dim, const double* phi_near, double* out,
-                   cudaStream_t s);
+                   cudaStream_t s, Own own, bool out_perm);
 
 // traverse.cu
 void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, int n0, Lists& lists,
@@ -165,11 +175,17 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& list
 
 // interact.cu
 void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, const Items& items,
-              double* phi_near, int* work_counter, cudaStream_t s);
+              double* phi_near, int* work_counter, cudaStream_t s, Own own);
 // all-pairs (direct_sum, summation.cpp:136-161): targets/sources AoS in input order.
 void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, const double* sxyz,
                      const double* sw, long long ns, double* out, DevBuf<double>& soa,
                      DevBuf<int4>& items, DevBuf<int2>& segs, int* work_counter, cudaStream_t s);
+
+// passes.cu: out[perm[t]] = phi_tree[t] (multi-GPU finish).
+void scatter_to_input(const DeviceTree& tgt, int dim, const double* phi_tree, double* out, cudaStream_t s);
+
+// probe.cu: DFMA-chain FP64 peak (TFLOP/s) of the current device.
+double probe_fp64_tflops(cudaStream_t s);
 
 // reference cluster ids (LIFO expansion order, cluster_tree.cpp:87-140) for export.
 std::vector<int> reference_ids(const std::vector<int>& parent, const std::vector<int>& depth,

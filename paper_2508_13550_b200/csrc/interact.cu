@@ -36,6 +36,8 @@ struct InteractParams {
     const double *sqx, *sqy, *sqz, *sqw;  // sources: proxy points + proxy weights
     double* out_p;  // phi_near (N_t x dim)
     double* out_q;  // proxy potentials (ncl_t x npp x dim)
+    const int* anchor;  // per item owner key (nullptr: every item is ours)
+    long long own_b, own_e;
 };
 
 template <class Op>
@@ -51,6 +53,10 @@ __global__ void __launch_bounds__(kIB) k_interact(InteractParams P, Op op) {
         const int it = item_sh;
         __syncthreads();
         if (it >= P.n_items) break;
+        if (P.anchor) {
+            const int a = P.anchor[it];
+            if (a >= 0 && (a < P.own_b || a >= P.own_e)) continue;  // another rank's target
+        }
         const int4 d = P.item[it];
         const bool tproxy = d.y < 0;
         const int tlen = tproxy ? -d.y : d.y;
@@ -185,8 +191,8 @@ void launch(const InteractParams& p, const Op& op, cudaStream_t s) {
 }  // namespace
 
 void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, const Items& items,
-              double* phi_near, int* work_counter, cudaStream_t s) {
-    InteractParams p;
+              double* phi_near, int* work_counter, cudaStream_t s, Own own) {
+    InteractParams p{};
     p.item = items.item;
     p.n_items = items.n_items;
     p.seg = items.seg;
@@ -207,6 +213,10 @@ void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src,
     p.sqw = src.qw;
     p.out_p = phi_near;
     p.out_q = tgt.qphi;
+    const bool everything = own.b <= 0 && own.e >= tgt.n;
+    p.anchor = everything ? nullptr : items.anchor.p;
+    p.own_b = own.b;
+    p.own_e = own.e;
     with_op(k, [&](auto op) { launch(p, op, s); });
 }
 

@@ -20,11 +20,19 @@ constexpr int kPassThreads = 128;
 constexpr int kP2mChunk = 64;
 
 // Leaf P2M (cluster_tree.cpp:180-191).  Internal clusters are written by k_m2m.
+// Which clusters a pass touches: mode 0 all, 1 owned at depth >= 1, 2 depth 0 only.
+__device__ __forceinline__ bool selected(const TreeView& t, int c, int mode, Own own) {
+    if (mode == 0) return true;
+    if (mode == 2) return t.depth[c] == 0;
+    return t.depth[c] >= 1 && t.begin[c] >= own.b && t.begin[c] < own.e;
+}
+
 __global__ void __launch_bounds__(kPassThreads)
-    k_p2m(TreeView t, Cheb cheb, const double* __restrict__ w, double* __restrict__ qw) {
+    k_p2m(TreeView t, Cheb cheb, const double* __restrict__ w, double* __restrict__ qw, int mode,
+          Own own) {
     extern __shared__ double sm[];
     const int c = blockIdx.x;
-    if (t.nchild[c] > 0) return;
+    if (t.nchild[c] > 0 || !selected(t, c, mode, own)) return;
     const int np = cheb.np, npp = np * np;
     double* WL = sm;                    // kP2mChunk x np   (w * Lx)
     double* LY = sm + kP2mChunk * np;   // kP2mChunk x np
@@ -75,11 +83,11 @@ __device__ __forceinline__ void mid_half(double a0, double a1, double& mid, doub
 
 // M2M (cluster_tree.cpp:192-216): pw = sum_children Axi * cw * Aeta^T, for one level.
 __global__ void __launch_bounds__(kPassThreads)
-    k_m2m(TreeView t, Cheb cheb, int first, double* __restrict__ qw) {
+    k_m2m(TreeView t, Cheb cheb, int first, double* __restrict__ qw, int mode, Own own) {
     extern __shared__ double sm[];
     const int c = first + blockIdx.x;
     const int nch = t.nchild[c];
-    if (nch == 0) return;
+    if (nch == 0 || !selected(t, c, mode, own)) return;
     const int np = cheb.np, npp = np * np;
     double* Ax = sm;             // At layout
     double* Ae = sm + npp;
@@ -124,11 +132,11 @@ __global__ void __launch_bounds__(kPassThreads)
 // L2L (cluster_tree.cpp:256-279), one CTA per child at level `first..`:
 // child[n1,n2,d] += sum_{m1,m2} Axi[m1,n1] Aeta[m2,n2] P[m1,m2,d], done separably.
 __global__ void __launch_bounds__(kPassThreads)
-    k_l2l(TreeView t, Cheb cheb, int first, int dim, double* __restrict__ qphi) {
+    k_l2l(TreeView t, Cheb cheb, int first, int dim, double* __restrict__ qphi, Own own) {
     extern __shared__ double sm[];
     const int ch = first + blockIdx.x;
     const int c = t.parent[ch];
-    if (c < 0) return;
+    if (c < 0 || t.begin[ch] < own.b || t.begin[ch] >= own.e) return;
     const int np = cheb.np, npp = np * np;
     double* Ax = sm;
     double* Ae = sm + npp;
@@ -163,12 +171,12 @@ __global__ void __launch_bounds__(kPassThreads)
 // out[perm[t]] = near[t] + sum_k Lx[k1] Ly[k2] P[k].
 __global__ void __launch_bounds__(kPassThreads)
     k_l2p(TreeView t, Cheb cheb, int dim, const double* __restrict__ qphi,
-          const double* __restrict__ near, double* __restrict__ out) {
+          const double* __restrict__ near, double* __restrict__ out, Own own, bool out_perm) {
     extern __shared__ double sm[];
     const int c = blockIdx.x;
     if (t.nchild[c] > 0) return;
     const int b = t.begin[c], e = t.end[c];
-    if (b == e) return;
+    if (b == e || b < own.b || b >= own.e) return;
     const int np = cheb.np, npp = np * np;
     for (int o = threadIdx.x; o < npp * dim; o += kPassThreads) sm[o] = qphi[(long long)c * npp * dim + o];
     __syncthreads();
@@ -188,40 +196,61 @@ __global__ void __launch_bounds__(kPassThreads)
                 for (int d = 0; d < dim; ++d) f[d] += bb * row[k2 * dim + d];
             }
         }
-        const long long dst = (long long)t.perm[p] * dim;
+        const long long dst = (long long)(out_perm ? t.perm[p] : p) * dim;
         for (int d = 0; d < dim; ++d) out[dst + d] = near[(long long)p * dim + d] + f[d];
     }
 }
 
+__global__ void k_scatter_out(long long n, int dim, const int* __restrict__ perm,
+                              const double* __restrict__ phi, double* __restrict__ out) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n * dim) return;
+    const long long t = g / dim;
+    const int d = int(g - t * dim);
+    out[(long long)perm[t] * dim + d] = phi[g];
+}
+
 }  // namespace
 
-void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s) {
+void scatter_to_input(const DeviceTree& tgt, int dim, const double* phi_tree, double* out, cudaStream_t s) {
+    const long long n = tgt.n * dim;
+    k_scatter_out<<<ceil_div(n, 256), 256, 0, s>>>(tgt.n, dim, tgt.perm, phi_tree, out);
+    CSFS_LAUNCH_CHECK();
+}
+
+void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s, int mode, Own own) {
     const TreeView v = src.view();
     const int np = cheb.np, npp = np * np;
-    src.qw.grow((size_t)src.ncl * npp);
+    if (mode != 2) {
+        src.qw.grow((size_t)src.ncl * npp);
+        if (mode == 1) CSFS_CK(cudaMemsetAsync(src.qw.p, 0, (size_t)src.ncl * npp * sizeof(double), s));
+    }
     const size_t sm_p2m = size_t(2) * kP2mChunk * np * sizeof(double);
-    k_p2m<<<src.ncl, kPassThreads, sm_p2m, s>>>(v, cheb, src.w, src.qw);
+    const int n_p2m = mode == 2 ? src.level_count[0] : src.ncl;  // depth 0 = ids 0..5
+    k_p2m<<<n_p2m, kPassThreads, sm_p2m, s>>>(v, cheb, src.w, src.qw, mode, own);
     CSFS_LAUNCH_CHECK();
     const size_t sm_m2m = size_t(3) * npp * sizeof(double);
-    for (int L = src.depth_max() - 1; L >= 0; --L) {
+    const int lo = mode == 1 ? 1 : 0;
+    const int hi = mode == 2 ? 0 : src.depth_max() - 1;
+    for (int L = hi; L >= lo; --L) {
         if (src.level_count[L] == 0) continue;
-        k_m2m<<<src.level_count[L], kPassThreads, sm_m2m, s>>>(v, cheb, src.level_first[L], src.qw);
+        k_m2m<<<src.level_count[L], kPassThreads, sm_m2m, s>>>(v, cheb, src.level_first[L], src.qw, mode, own);
         CSFS_LAUNCH_CHECK();
     }
 }
 
 void downward_pass(DeviceTree& tgt, const Cheb& cheb, int dim, const double* phi_near, double* out,
-                   cudaStream_t s) {
+                   cudaStream_t s, Own own, bool out_perm) {
     const TreeView v = tgt.view();
     const int np = cheb.np, npp = np * np;
     const size_t sm_l2l = size_t(2 * npp + npp * dim) * sizeof(double);
     for (int L = 1; L <= tgt.depth_max(); ++L) {
         if (tgt.level_count[L] == 0) continue;
-        k_l2l<<<tgt.level_count[L], kPassThreads, sm_l2l, s>>>(v, cheb, tgt.level_first[L], dim, tgt.qphi);
+        k_l2l<<<tgt.level_count[L], kPassThreads, sm_l2l, s>>>(v, cheb, tgt.level_first[L], dim, tgt.qphi, own);
         CSFS_LAUNCH_CHECK();
     }
     const size_t sm_l2p = size_t(npp) * dim * sizeof(double);
-    k_l2p<<<tgt.ncl, kPassThreads, sm_l2p, s>>>(v, cheb, dim, tgt.qphi, phi_near, out);
+    k_l2p<<<tgt.ncl, kPassThreads, sm_l2p, s>>>(v, cheb, dim, tgt.qphi, phi_near, out, own, out_perm);
     CSFS_LAUNCH_CHECK();
 }
 

@@ -75,9 +75,12 @@ __global__ void k_fill(const int2* __restrict__ l, long long n, int key_off, int
 }
 
 // Per work item: canonical order of its sources, then segment descriptors.
+// anchor = first target particle of the item's cluster (owner test for the multi-GPU
+// partition), or -1 for depth-0 targets, which every rank evaluates redundantly.
 __global__ void k_items(int n_items, int ncl_t, const int* __restrict__ keys,
                         const int* __restrict__ cnt, const int* __restrict__ off, long long* code,
-                        int2* seg, int4* item, const TreeView T, const TreeView S) {
+                        int2* seg, int4* item, int* anchor, double* cost, const TreeView T,
+                        const TreeView S) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_items) return;
     const int key = keys[i];
@@ -92,14 +95,24 @@ __global__ void k_items(int n_items, int ncl_t, const int* __restrict__ keys,
         }
         c[j + 1] = v;
     }
+    long long src_pts = 0;
     for (int a = 0; a < n; ++a) {
         const int type = int(c[a] >> 32);
         const int s = int(c[a] & 0xffffffffll);
-        if (type == 0 || type == 2) seg[b + a] = make_int2(S.begin[s], S.end[s] - S.begin[s]);
-        else seg[b + a] = make_int2(s * S.npp, -S.npp);
+        if (type == 0 || type == 2) {
+            seg[b + a] = make_int2(S.begin[s], S.end[s] - S.begin[s]);
+            src_pts += S.end[s] - S.begin[s];
+        } else {
+            seg[b + a] = make_int2(s * S.npp, -S.npp);
+            src_pts += S.npp;
+        }
     }
-    if (key < ncl_t) item[i] = make_int4(T.begin[key], T.end[key] - T.begin[key], b, b + n);
-    else item[i] = make_int4((key - ncl_t) * T.npp, -T.npp, b, b + n);
+    const int t = key < ncl_t ? key : key - ncl_t;
+    const int tl = key < ncl_t ? T.end[t] - T.begin[t] : T.npp;
+    if (key < ncl_t) item[i] = make_int4(T.begin[t], tl, b, b + n);
+    else item[i] = make_int4(t * T.npp, -T.npp, b, b + n);
+    anchor[i] = T.depth[t] == 0 ? -1 : T.begin[t];
+    cost[i] = double(tl) * double(src_pts);
 }
 
 }  // namespace
@@ -208,6 +221,8 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, I
     it.code.grow(std::max<long long>(it.n_entries, 1));
     it.seg.grow(std::max<long long>(it.n_entries, 1));
     it.item.grow(std::max(it.n_items, 1));
+    it.anchor.grow(std::max(it.n_items, 1));
+    it.cost.grow(std::max(it.n_items, 1));
     for (int k = 0; k < 4; ++k) {
         if (L.n[k] == 0) continue;
         k_fill<<<ceil_div(L.n[k], kThreads), kThreads, 0, s>>>(L.l[k], L.n[k], k <= 1 ? 0 : ncl_t, k,
@@ -216,7 +231,8 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, I
     }
     if (it.n_items) {
         k_items<<<ceil_div(it.n_items, 128), 128, 0, s>>>(it.n_items, ncl_t, it.keys, it.cnt, it.off,
-                                                         it.code, it.seg, it.item, T, S);
+                                                         it.code, it.seg, it.item, it.anchor, it.cost,
+                                                         T, S);
         CSFS_LAUNCH_CHECK();
     }
 }

@@ -148,6 +148,15 @@ def lib() -> C.CDLL:
         L.csfs_b200_tree_export.argtypes = [P, I, P, P, P, P]
         L.csfs_b200_lists_export.argtypes = [P, C.POINTER(C.c_longlong), P, P, P, P]
         L.csfs_b200_proxy_weights_export.argtypes = [P, P]
+        L.csfs_b200_kernel_launches.restype = C.c_uint64
+        L.csfs_b200_kernel_launches.argtypes = []
+        L.csfs_b200_probe_fp64.argtypes = [P, C.POINTER(C.c_double)]
+        L.csfs_b200_part_plan.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), C.POINTER(_CConfig), P]
+        L.csfs_b200_part_units.argtypes = [P, I, C.POINTER(I), P, P, P]
+        L.csfs_b200_part_sizes.argtypes = [P, C.POINTER(S), C.POINTER(S)]
+        L.csfs_b200_part_upward.argtypes = [P, C.c_longlong, C.c_longlong, P]
+        L.csfs_b200_part_eval.argtypes = [P, C.c_longlong, C.c_longlong, P, P]
+        L.csfs_b200_part_finish.argtypes = [P, P, P]
         _lib = L
     return _lib
 
@@ -200,13 +209,17 @@ class Engine:
 
     # --- reference API mirror --------------------------------------------------------
     def csfmm_sum(self, targets: ParticleSet, sources: ParticleSet, kernel: Kernel,
-                  config: TraversalConfig, stats: SumStats | None = None) -> PotentialField:
+                  config: TraversalConfig, stats: SumStats | None = None,
+                  out: np.ndarray | None = None) -> PotentialField:
+        """`out` (optional, n*out_dim float64, e.g. a pinned buffer) receives the result."""
         tx = np.ascontiguousarray(targets.positions, dtype=np.float64)
         sx = tx if sources.positions is targets.positions else np.ascontiguousarray(sources.positions, dtype=np.float64)
         sw = np.ascontiguousarray(sources.weights, dtype=np.float64)
         if sw.shape[0] != sx.shape[0]:
             raise ValueError("weight count does not match particle count")
-        out = np.empty(tx.shape[0] * kernel.out_dim())
+        if out is None:
+            out = np.empty(tx.shape[0] * kernel.out_dim())
+        assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == tx.shape[0] * kernel.out_dim()
         st = stats if stats is not None else SumStats()
         self._check(self._lib.csfs_b200_csfmm(self._h, _ptr(tx), tx.shape[0], _ptr(sx), _ptr(sw), sx.shape[0],
                                               C.byref(_ckernel(kernel)), C.byref(_cconfig(config)), _ptr(out),
@@ -272,11 +285,50 @@ class Engine:
         self._check(self._lib.csfs_b200_lists_export(self._h, counts, *[_ptr(b) for b in bufs]))
         return dict(zip(["pp", "pc", "cp", "cc"], bufs))
 
+    # --- multi-GPU partition phases (see distributed.py) ------------------------------
+    def part_plan(self, tgt_xyz_ptr, nt, src_xyz_ptr, src_w_ptr, ns, kernel, config, stream=0):
+        self._check(self._lib.csfs_b200_part_plan(
+            self._h, C.c_void_p(tgt_xyz_ptr), nt, C.c_void_p(src_xyz_ptr), C.c_void_p(src_w_ptr), ns,
+            C.byref(_ckernel(kernel)), C.byref(_cconfig(config)), C.c_void_p(stream)))
+
+    def part_units(self, which: int):
+        n = C.c_int()
+        self._check(self._lib.csfs_b200_part_units(self._h, which, C.byref(n), None, None, None))
+        b = np.empty(n.value, np.int64)
+        e = np.empty(n.value, np.int64)
+        c = np.empty(n.value)
+        self._check(self._lib.csfs_b200_part_units(self._h, which, C.byref(n), _ptr(b), _ptr(e), _ptr(c)))
+        return b, e, c
+
+    def part_sizes(self) -> tuple[int, int]:
+        a, b = C.c_size_t(), C.c_size_t()
+        self._check(self._lib.csfs_b200_part_sizes(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def part_upward(self, b: int, e: int, pw_ptr: int):
+        self._check(self._lib.csfs_b200_part_upward(self._h, b, e, C.c_void_p(pw_ptr)))
+
+    def part_eval(self, b: int, e: int, pw_ptr: int, phi_ptr: int):
+        self._check(self._lib.csfs_b200_part_eval(self._h, b, e, C.c_void_p(pw_ptr), C.c_void_p(phi_ptr)))
+
+    def part_finish(self, phi_ptr: int, out_ptr: int):
+        self._check(self._lib.csfs_b200_part_finish(self._h, C.c_void_p(phi_ptr), C.c_void_p(out_ptr)))
+
+    def probe_fp64_tflops(self) -> float:
+        v = C.c_double()
+        self._check(self._lib.csfs_b200_probe_fp64(self._h, C.byref(v)))
+        return v.value
+
     def proxy_weights_export(self) -> np.ndarray:
         ncl, _, _, npp = self.tree_info(1)
         pw = np.empty((ncl, npp))
         self._check(self._lib.csfs_b200_proxy_weights_export(self._h, _ptr(pw)))
         return pw
+
+
+def kernel_launches() -> int:
+    """Engine kernels launched by this process so far."""
+    return int(lib().csfs_b200_kernel_launches())
 
 
 _default: Engine | None = None

@@ -1,0 +1,57 @@
+"""Multi-GPU target partitioning on ONE GPU: the R ranks are emulated one after the other
+(each rank's phase is an independent launch; the all-reduces are done here on the device
+by summing the per-rank buffers), so nothing waits on another rank.  The result must be
+BITWISE identical to the single-GPU evaluation for every R (each target is evaluated by
+exactly one rank in the single-GPU order; every reduced slot has one non-zero term)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2508_13550_b200 import Kernel, TraversalConfig, configs
+from paper_2508_13550_b200.distributed import plan_partition
+
+pytestmark = pytest.mark.gpu
+
+
+def emulate(engine, xyz, w, kernel, cfg, world):
+    dev = xyz.device
+    s = torch.cuda.current_stream(dev).cuda_stream
+    engine.part_plan(xyz.data_ptr(), xyz.shape[0], xyz.data_ptr(), w.data_ptr(), xyz.shape[0], kernel, cfg, s)
+    plans = [plan_partition(engine, r, world) for r in range(world)]
+    n_pw, n_phi = engine.part_sizes()
+    pws = [torch.empty(n_pw, dtype=torch.float64, device=dev) for _ in plans]
+    for p, buf in zip(plans, pws):
+        engine.part_upward(*p.source_range, buf.data_ptr())
+    pw = torch.stack(pws).sum(0)  # the all-reduce
+    phis = [torch.empty(n_phi, dtype=torch.float64, device=dev) for _ in plans]
+    for p, buf in zip(plans, phis):
+        engine.part_eval(*p.target_range, pw.data_ptr(), buf.data_ptr())
+    phi = torch.stack(phis).sum(0)
+    out = torch.empty(xyz.shape[0] * kernel.out_dim(), dtype=torch.float64, device=dev)
+    engine.part_finish(phi.data_ptr(), out.data_ptr())
+    return out, plans, pws
+
+
+@pytest.mark.parametrize("name,level,kname", [("c1", 5, None), ("c3", 6, None), ("c4", 6, None)])
+def test_partition_bitwise(engine, name, level, kname):
+    wl = configs.make(name, level=level)
+    dev = torch.device("cuda", 0)
+    xyz = torch.from_numpy(wl.xyz).to(dev)
+    w = torch.from_numpy(wl.weights).to(dev)
+    k = Kernel.parse(kname or wl.kernel)
+    cfg = TraversalConfig(mac=wl.mac, degree=wl.degree, n0=wl.n0)
+    ref_out = torch.empty(wl.n * k.out_dim(), dtype=torch.float64, device=dev)
+    engine.csfmm_device(xyz.data_ptr(), wl.n, xyz.data_ptr(), w.data_ptr(), wl.n, k, cfg, ref_out.data_ptr(),
+                        torch.cuda.current_stream().cuda_stream)
+    want = ref_out.cpu().numpy()
+    want_pw = engine.proxy_weights_export()
+    for world in (1, 2, 4, 8):
+        got, plans, pws = emulate(engine, xyz, w, k, cfg, world)
+        # every proxy weight slot at depth >= 1 has exactly one owner
+        nz = torch.stack([(p != 0) for p in pws]).sum(0)
+        assert int(nz.max()) <= 1, f"world={world}: a proxy weight has {int(nz.max())} owners"
+        np.testing.assert_array_equal(got.cpu().numpy(), want, err_msg=f"world={world}")
+        # target ranges tile [0, N) in order
+        rngs = [p.target_range for p in plans if p.target_range[1] > p.target_range[0]]
+        assert rngs[0][0] == 0 and rngs[-1][1] == wl.n
+        assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
