@@ -92,16 +92,16 @@ def partitioned_csfmm(engine, tgt_xyz, src_xyz, src_w, kernel, config, out, grou
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     bufs = bufs if bufs is not None else getattr(engine, "_exchange", None) or ExchangeBuffers()
     engine._exchange = bufs
-    stream = torch.cuda.current_stream(tgt_xyz.device).cuda_stream
-    engine.part_plan(tgt_xyz.data_ptr(), tgt_xyz.shape[0], src_xyz.data_ptr(), src_w.data_ptr(),
-                     src_xyz.shape[0], kernel, config, stream)
+    dev = tgt_xyz.device
+    stream = torch.cuda.current_stream(dev).cuda_stream if dev.type == "cuda" else 0
+    engine.part_plan(tgt_xyz, tgt_xyz.shape[0], src_xyz, src_w, src_xyz.shape[0], kernel, config, stream)
     plan = plan_partition(engine, rank, world)
-    pw, phi = bufs.ensure(*engine.part_sizes(), tgt_xyz.device)
-    engine.part_upward(*plan.source_range, pw.data_ptr())
+    pw, phi = bufs.ensure(*engine.part_sizes(), dev)
+    engine.part_upward(*plan.source_range, pw)
     if allreduce is not None:
         allreduce(pw)
-    engine.part_eval(*plan.target_range, pw.data_ptr(), phi.data_ptr())
+    engine.part_eval(*plan.target_range, pw, phi)
     if allreduce is not None:
         allreduce(phi)
-    engine.part_finish(phi.data_ptr(), out.data_ptr())
+    engine.part_finish(phi, out)
     return plan

@@ -165,6 +165,11 @@ def _ptr(a: np.ndarray) -> C.c_void_p:
     return C.c_void_p(a.ctypes.data)
 
 
+def _dptr(x) -> C.c_void_p:
+    """Device pointer from a torch tensor (data_ptr) or a raw integer address."""
+    return C.c_void_p(x.data_ptr() if hasattr(x, "data_ptr") else int(x))
+
+
 def _ckernel(k: Kernel) -> _CKernel:
     return _CKernel(int(k.kind), k.sal.a1, k.sal.b0, k.sal.b1, k.sal.rho_ratio)
 
@@ -286,9 +291,10 @@ class Engine:
         return dict(zip(["pp", "pc", "cp", "cc"], bufs))
 
     # --- multi-GPU partition phases (see distributed.py) ------------------------------
-    def part_plan(self, tgt_xyz_ptr, nt, src_xyz_ptr, src_w_ptr, ns, kernel, config, stream=0):
+    def part_plan(self, tgt_xyz, nt, src_xyz, src_w, ns, kernel, config, stream=0):
+        """Arguments are device tensors or raw device addresses."""
         self._check(self._lib.csfs_b200_part_plan(
-            self._h, C.c_void_p(tgt_xyz_ptr), nt, C.c_void_p(src_xyz_ptr), C.c_void_p(src_w_ptr), ns,
+            self._h, _dptr(tgt_xyz), nt, _dptr(src_xyz), _dptr(src_w), ns,
             C.byref(_ckernel(kernel)), C.byref(_cconfig(config)), C.c_void_p(stream)))
 
     def part_units(self, which: int):
@@ -305,14 +311,14 @@ class Engine:
         self._check(self._lib.csfs_b200_part_sizes(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
-    def part_upward(self, b: int, e: int, pw_ptr: int):
-        self._check(self._lib.csfs_b200_part_upward(self._h, b, e, C.c_void_p(pw_ptr)))
+    def part_upward(self, b: int, e: int, pw):
+        self._check(self._lib.csfs_b200_part_upward(self._h, b, e, _dptr(pw)))
 
-    def part_eval(self, b: int, e: int, pw_ptr: int, phi_ptr: int):
-        self._check(self._lib.csfs_b200_part_eval(self._h, b, e, C.c_void_p(pw_ptr), C.c_void_p(phi_ptr)))
+    def part_eval(self, b: int, e: int, pw, phi):
+        self._check(self._lib.csfs_b200_part_eval(self._h, b, e, _dptr(pw), _dptr(phi)))
 
-    def part_finish(self, phi_ptr: int, out_ptr: int):
-        self._check(self._lib.csfs_b200_part_finish(self._h, C.c_void_p(phi_ptr), C.c_void_p(out_ptr)))
+    def part_finish(self, phi, out):
+        self._check(self._lib.csfs_b200_part_finish(self._h, _dptr(phi), _dptr(out)))
 
     def probe_fp64_tflops(self) -> float:
         v = C.c_double()

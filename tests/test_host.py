@@ -1,0 +1,97 @@
+"""CPU: host-side pieces — the C-ABI library loads and exports exactly what
+include/csfs_b200.h declares, the Python mirror of the reference API behaves like the
+reference (argument meaning, defaults, error messages), the product fails loudly
+without a GPU, and the input generators reproduce the reference's grids bitwise."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import ref
+from paper_2508_13550_b200 import Kernel, KernelKind, SalParams, TraversalConfig, configs, engine
+from paper_2508_13550_b200.grids import cubed_sphere, real_sph_harm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "csfs_b200.h")).read()
+    return sorted(set(re.findall(r"CSFS_B200_API\s+[\w\s\*]+?\b(csfs_b200_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    syms = header_symbols()
+    assert len(syms) >= 18
+    lib = ctypes.CDLL(engine.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), f"{s} declared in include/csfs_b200.h but not exported"
+
+
+def test_library_hides_internal_symbols():
+    out = os.popen(f"nm -D --defined-only {engine.LIB_PATH}").read()
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert exported == set(header_symbols())
+
+
+def test_fails_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        engine.Engine(0)
+
+
+def test_reference_api_mirror():
+    assert Kernel.parse("laplace").kind == KernelKind.Laplace
+    assert Kernel.parse("biot_savart").out_dim() == 3
+    assert not Kernel.parse("biharmonic").singular_at_coincidence()
+    with pytest.raises(ValueError, match="unknown kernel: fmm3d"):
+        Kernel.parse("fmm3d")
+    cfg = TraversalConfig()
+    assert (cfg.mac, cfg.degree, cfg.n0, cfg.shrink) == (0.7, 6, -1, True)  # summation.hpp:22-31
+    assert cfg.resolved_n0() == 144
+    assert TraversalConfig(degree=10, n0=256).resolved_n0() == 256
+    s = SalParams()
+    assert (s.a1, s.b0, s.b1, s.rho_ratio) == (-2.7, -6.21196, 6.1, 1025.0 / 5517.0)  # kernels.hpp:18-23
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("level", [0, 3, 5, 8])
+def test_cubed_sphere_matches_reference_bitwise(level):
+    xyz, a = cubed_sphere(level)
+    rx, ra = ref.grid("cubed_sphere", level)
+    np.testing.assert_array_equal(xyz, rx)
+    np.testing.assert_array_equal(a, ra)
+
+
+def test_cubed_sphere_properties():
+    xyz, a = cubed_sphere(5)
+    assert xyz.shape == (6144, 3)
+    np.testing.assert_allclose(np.linalg.norm(xyz, axis=1), 1.0, atol=1e-15)
+    assert a.sum() == pytest.approx(4 * np.pi, rel=1e-12)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_real_sph_harm_matches_reference():
+    xyz, _ = cubed_sphere(4)
+    for l, m in [(1, 0), (4, 3), (7, -5), (32, 17), (20, -20)]:
+        np.testing.assert_allclose(real_sph_harm(l, m, xyz), ref.sph_harm(l, m, xyz), rtol=1e-11, atol=1e-13)
+
+
+def test_configs_deterministic_and_shaped():
+    for name, n in [("c1", 6144), ("c2", 6 * 4 ** 5), ("c3", 6 * 4 ** 5), ("c4", 6 * 4 ** 5), ("c5", 6 * 4 ** 5)]:
+        a = configs.make(name, level=None if name == "c1" else 5)
+        b = configs.make(name, level=None if name == "c1" else 5)
+        assert a.n == n
+        np.testing.assert_array_equal(a.weights, b.weights)
+    c3 = configs.make("c3", level=5)
+    assert abs((c3.f * c3.areas).sum()) < 1e-12  # zero mean
+    c5 = configs.make("c5", level=5)
+    assert 0.65 < c5.meta["ocean_fraction"] < 0.75
+    c1 = configs.make("c1")
+    assert (c1.kernel, c1.degree, c1.mac, c1.n0) == ("laplace", 8, 0.7, 64)
+    c5 = configs.make("c5", level=5)
+    assert (c5.kernel, c5.degree, c5.mac, c5.n0) == ("sal", 10, 0.6, 256)
