@@ -136,16 +136,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def load_traffic():
-    """dram bytes per k_interact launch from the newest committed ncu summary (or None)."""
-    files = sorted(glob.glob(os.path.join(HERE, "profiles", "*interact*ncu*.json")))
+def load_ncu(kernel_tag: str):
+    """Newest committed ncu summary of the evaluation kernel (profiles/*interact_<tag>*ncu*.json)."""
+    files = sorted(glob.glob(os.path.join(HERE, "profiles", f"*interact_{kernel_tag}*ncu*.json")))
     if not files:
-        return None, None
+        return {}, None
     try:
-        d = json.load(open(files[-1]))
-        return d.get("dram_bytes_per_launch"), os.path.relpath(files[-1], HERE)
+        return json.load(open(files[-1])), os.path.relpath(files[-1], HERE)
     except Exception:
-        return None, None
+        return {}, None
 
 
 def run_reference(args):
@@ -257,14 +256,25 @@ def main():
         t_int = statistics.mean(s.t_interact for s in stats)
         flops = evals * FLOP_PER_PAIR[wl.kernel]
         achieved = flops / t_int / 1e12
-        traffic, traffic_src = load_traffic()
-        roof = {"bound": "fp64", "kernel": "k_interact<OpSal> (PP+PC+CP+CC)", "achieved": achieved,
+        ncu, ncu_src = load_ncu({"sal": "sal", "laplace": "laplace", "biharmonic": "biharmonic",
+                                 "biot_savart": "bs"}[wl.kernel])
+        traffic = ncu.get("dram_bytes_per_launch")
+        exec_fpp = ncu.get("fp64_flop_per_pair_executed")
+        roof = {"bound": "fp64", "kernel": f"k_interact<Op{wl.kernel}> (PP+PC+CP+CC)", "achieved": achieved,
                 "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                "traffic": traffic, "traffic_source": traffic_src,
+                "traffic": traffic, "traffic_source": ncu_src,
+                "algorithmic_flop_per_pair": FLOP_PER_PAIR[wl.kernel],
+                "algorithmic_convention": "SURVEY.md §8d: reference formula as executed by sm_100a libdevice "
+                                          "(DFMA=2); our functor computes the same value with fewer FP64 ops, "
+                                          "so frac can exceed 1 — see executed_* for pipe-level utilisation",
+                "executed_flop_per_pair": exec_fpp,
+                "executed_tflops": (evals * exec_fpp / t_int / 1e12) if exec_fpp else None,
+                "executed_frac": (evals * exec_fpp / t_int / 1e12 / fp64_peak) if exec_fpp else None,
+                "fp64_pipe_active_pct_ncu": ncu.get("fp64_pipe_active_pct"),
                 "peak_source": "measured DFMA-chain probe (csfs_b200_probe_fp64) on this GPU; "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "frac_of_nominal_37.2": achieved / NOMINAL_FP64_TFLOPS,
-                "flop_per_pair": FLOP_PER_PAIR[wl.kernel], "pair_evals_per_launch": evals,
+                "pair_evals_per_launch": evals,
                 "kernel_ms": t_int * 1e3, "share_of_step": t_int / (ms_per_step * 1e-3),
                 "phases_ms": {kk: 1e3 * statistics.mean(getattr(s, kk) for s in stats)
                               for kk in ("t_tree_build", "t_upward", "t_lists", "t_interact", "t_downward", "t_total")}}
@@ -322,6 +332,7 @@ def main():
                 "clocks": clk.summary()}
         if roof:
             line["fp64_frac_p2p_m2l"] = roof["frac"]
+            line["fp64_frac_p2p_m2l_executed"] = roof["executed_frac"]
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

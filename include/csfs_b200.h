@@ -148,6 +148,14 @@ CSFS_B200_API int csfs_b200_part_finish(csfs_b200_ctx* ctx, const double* phi_re
 /* --- diagnostics ------------------------------------------------------------------------ */
 /* Number of engine kernels launched by this process so far (all contexts). */
 CSFS_B200_API uint64_t csfs_b200_kernel_launches(void);
+/* The device kernel functor on n (x_i, y_i) pairs (host arrays, n x 3 each): the
+ * reference's guarded per-pair value K(x_i, y_i) (0 where the coincidence guard skips),
+ * out n x out_dim — Kernel::try_eval (kernels.cpp) known-answer checks on the GPU path. */
+CSFS_B200_API int csfs_b200_eval_pairs(csfs_b200_ctx* ctx, const csfs_b200_kernel* kernel,
+                                       const double* x, const double* y, size_t n, double* out);
+/* The device elementary functions on n host values: fn 0 log, 1 rsqrt, 2 rcp, 3 dilog. */
+CSFS_B200_API int csfs_b200_eval_math(csfs_b200_ctx* ctx, int fn, const double* x, size_t n,
+                                      double* out);
 /* Measured FP64 FMA-pipe peak of the context's device in TFLOP/s (DFMA = 2 flops). */
 CSFS_B200_API int csfs_b200_probe_fp64(csfs_b200_ctx* ctx, double* tflops);
 

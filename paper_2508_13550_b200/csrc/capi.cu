@@ -31,6 +31,7 @@ struct csfs_b200_ctx {
     DevBuf<double> d_soa;
     DevBuf<int4> d_items;
     DevBuf<int2> d_segs;
+    DevBuf<double2> log_tab;  // fastmath.cuh table, uploaded once per context
     cudaEvent_t ev[8] = {};
     Cheb cheb{};
     KernelSpec kspec;
@@ -166,7 +167,7 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     CSFS_CK(cudaMemsetAsync(c->phi_near.p, 0, nt * dim * sizeof(double), s));
     CSFS_CK(cudaMemsetAsync(T.qphi.p, 0, size_t(T.ncl) * T.npp * dim * sizeof(double), s));
     c->counter.grow(4);
-    interact(ks, T, S, c->items, c->phi_near, c->counter, s, Own{0, (long long)nt});
+    interact(ks, T, S, c->items, c->phi_near, c->counter, c->log_tab, s, Own{0, (long long)nt});
     CSFS_CK(cudaEventRecord(ev[4], s));
 
     downward_pass(T, c->cheb, dim, c->phi_near, out, s, Own{0, (long long)nt}, true);
@@ -259,6 +260,10 @@ int csfs_b200_create(csfs_b200_ctx** out, int device) {
         CSFS_CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
         for (auto& e : c->ev) CSFS_CK(cudaEventCreate(&e));
         CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
+        std::vector<double2> tab(2 * kLogTab);
+        make_log_table(tab.data());
+        c->log_tab.grow(2 * kLogTab);
+        CSFS_CK(cudaMemcpy(c->log_tab.p, tab.data(), 2 * kLogTab * sizeof(double2), cudaMemcpyHostToDevice));
     });
     if (rc != CSFS_B200_OK) {
         // keep the context alive only to report the error? The caller gets NULL.
@@ -324,7 +329,7 @@ int csfs_b200_direct_device(csfs_b200_ctx* c, const double* txyz, size_t nt, con
         const KernelSpec ks = to_spec(k);
         c->counter.grow(4);
         direct_allpairs(ks, txyz, (long long)nt, sxyz, sw, (long long)ns, out, c->d_soa, c->d_items,
-                        c->d_segs, c->counter, pick(c, stream));
+                        c->d_segs, c->counter, c->log_tab, pick(c, stream));
     });
 }
 
@@ -346,7 +351,7 @@ int csfs_b200_direct(csfs_b200_ctx* c, const double* txyz, size_t nt, const doub
         if (nout) CSFS_CK(cudaMemsetAsync(c->h_out.p, 0, nout * sizeof(double), s));
         c->counter.grow(4);
         direct_allpairs(ks, c->h_txyz.p, (long long)nt, c->h_sxyz.p, c->h_w.p, (long long)ns, c->h_out.p,
-                        c->d_soa, c->d_items, c->d_segs, c->counter, s);
+                        c->d_soa, c->d_items, c->d_segs, c->counter, c->log_tab, s);
         if (nout) CSFS_CK(cudaMemcpyAsync(out, c->h_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaStreamSynchronize(s));
     });
@@ -560,7 +565,7 @@ int csfs_b200_part_eval(csfs_b200_ctx* c, long long tgt_b, long long tgt_e, cons
         CSFS_CK(cudaMemsetAsync(phi, 0, nt * dim * sizeof(double), s));
         CSFS_CK(cudaMemsetAsync(T.qphi.p, 0, size_t(T.ncl) * T.npp * dim * sizeof(double), s));
         c->counter.grow(4);
-        interact(c->kspec, T, S, c->items, c->phi_near, c->counter, s, Own{tgt_b, tgt_e});
+        interact(c->kspec, T, S, c->items, c->phi_near, c->counter, c->log_tab, s, Own{tgt_b, tgt_e});
         downward_pass(T, c->cheb, dim, c->phi_near, phi, s, Own{tgt_b, tgt_e}, false);
     });
 }
@@ -571,6 +576,37 @@ int csfs_b200_part_finish(csfs_b200_ctx* c, const double* phi_reduced, double* o
         scatter_to_input(c->ttree, c->dim, phi_reduced, out, c->part_stream);
         CSFS_CK(cudaStreamSynchronize(c->part_stream));
         c->have_state = true;
+    });
+}
+
+int csfs_b200_eval_pairs(csfs_b200_ctx* c, const csfs_b200_kernel* k, const double* x, const double* y,
+                         size_t n, double* out) {
+    return guarded(c, [&] {
+        const KernelSpec ks = to_spec(k);
+        DevBuf<double> d;
+        d.grow(std::max<size_t>(n * 9, 1));
+        cudaStream_t s = c->own;
+        const size_t nout = n * ks.out_dim();
+        if (n) {
+            CSFS_CK(cudaMemcpyAsync(d.p, x, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+            CSFS_CK(cudaMemcpyAsync(d.p + 3 * n, y, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        eval_pairs(ks, d.p, d.p + 3 * n, (long long)n, d.p + 6 * n, c->log_tab, s);
+        if (n) CSFS_CK(cudaMemcpyAsync(out, d.p + 6 * n, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
+    });
+}
+
+int csfs_b200_eval_math(csfs_b200_ctx* c, int fn, const double* x, size_t n, double* out) {
+    return guarded(c, [&] {
+        if (fn < 0 || fn > 3) throw InvalidArgument("fn must be 0 (log), 1 (rsqrt), 2 (rcp) or 3 (dilog)");
+        DevBuf<double> d;
+        d.grow(std::max<size_t>(2 * n, 1));
+        cudaStream_t s = c->own;
+        if (n) CSFS_CK(cudaMemcpyAsync(d.p, x, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        eval_math(fn, d.p, (long long)n, d.p + n, c->log_tab, s);
+        if (n) CSFS_CK(cudaMemcpyAsync(out, d.p + n, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
     });
 }
 

@@ -23,6 +23,8 @@ constexpr double kCoincidenceTol = 1e-14;  // kernels.hpp:28
 constexpr double kNodeTol = 1e-14;         // interpolation.cpp:8
 constexpr int kMaxDepth = 60;              // cluster_tree.cpp:11
 constexpr double kMinExtent = 1e-13;       // cluster_tree.cpp:12
+constexpr int kLogTabBits = 8;             // fastmath.cuh log table: 256 entries
+constexpr int kLogTab = 1 << kLogTabBits;
 
 // Error classes that map onto the C-ABI return codes (include/csfs_b200.h).
 struct InvalidArgument : std::runtime_error {

@@ -175,11 +175,18 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& list
 
 // interact.cu
 void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, const Items& items,
-              double* phi_near, int* work_counter, cudaStream_t s, Own own);
+              double* phi_near, int* work_counter, const double2* log_tab, cudaStream_t s, Own own);
 // all-pairs (direct_sum, summation.cpp:136-161): targets/sources AoS in input order.
 void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, const double* sxyz,
                      const double* sw, long long ns, double* out, DevBuf<double>& soa,
-                     DevBuf<int4>& items, DevBuf<int2>& segs, int* work_counter, cudaStream_t s);
+                     DevBuf<int4>& items, DevBuf<int2>& segs, int* work_counter,
+                     const double2* log_tab, cudaStream_t s);
+// diagnostics: guarded scaled kernel values of (x_i, y_i) pairs; fastmath functions
+// (fn 0 log, 1 rsqrt, 2 rcp, 3 dilog).
+void eval_pairs(const KernelSpec& k, const double* x, const double* y, long long n, double* out,
+                const double2* log_tab, cudaStream_t s);
+void eval_math(int fn, const double* x, long long n, double* out, const double2* log_tab, cudaStream_t s);
+void make_log_table(double2* tab);
 
 // passes.cu: out[perm[t]] = phi_tree[t] (multi-GPU finish).
 void scatter_to_input(const DeviceTree& tgt, int dim, const double* phi_tree, double* out, cudaStream_t s);

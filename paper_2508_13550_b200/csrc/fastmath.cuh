@@ -1,0 +1,79 @@
+// FP64 elementary functions for the evaluation kernel, sized to the FP64 pipe budget.
+//
+// The evaluation phases are FP64-issue bound.  libdevice's log is
+// ~28 FP64 instructions, sqrt and a/b ~8 each; the kernel functors need:
+//   log   -> Tang-style table method: x = 2^e m, m r_i = 1 + t with |t| <= 2^-8 from a
+//            256-entry shared-memory table {r_i, -ln r_i split hi (42-bit) + lo}, so
+//            e ln2_hi + L_hi is exact; log1p(t) by a degree-7 polynomial.  The two
+//            intervals touching x = 1 use r = 1 and r = 1/2 exactly, so t is exact and
+//            the result keeps full relative accuracy where log(x) ~ 0 — branch-free.
+//            13 FP64 instructions, <= 1 ulp (mpmath check in tests/test_gpu_numerics.py).
+//   rsqrt -> MUFU.RSQ64H seed + one cubic-convergent correction (5 FP64), <= 2 ulp.
+//   rcp   -> MUFU.RCP64H seed + one cubic-convergent correction (3 FP64), <= 2 ulp.
+// Arguments are finite positive normals (the coincidence guard keeps 1 - x.y >= 1e-14).
+#pragma once
+
+#include "common.cuh"
+
+namespace csfs_b200 {
+
+// Table layout (host-built by make_log_table, copied to shared memory per CTA):
+// tab[i] = {r_i, L_hi_i}, tab[kLogTab + i].x = L_lo_i.
+struct LogTable {
+    const double2* rl;  // kLogTab
+    const double* lo;   // kLogTab
+};
+
+__device__ __forceinline__ double fast_log(double x, const LogTable& tb) {
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    const int e = ((hi >> 20) & 0x7ff) - 1023;
+    const int i = (hi >> (20 - kLogTabBits)) & (kLogTab - 1);
+    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    const double2 rl = tb.rl[i];
+    // |t| <= 2^-8; exact for the two intervals touching x = 1 (r = 1 and r = 1/2)
+    const double t = fma(m, rl.x, -1.0);
+    double p = 1.0 / 7.0;
+    p = fma(p, t, -1.0 / 6.0);
+    p = fma(p, t, 1.0 / 5.0);
+    p = fma(p, t, -1.0 / 4.0);
+    p = fma(p, t, 1.0 / 3.0);
+    p = fma(p, t, -1.0 / 2.0);
+    const double ed = double(e);
+    constexpr double kLn2Hi = 0x1.62e42fefa3800p-1;  // 42 significant bits: e*kLn2Hi exact
+    constexpr double kLn2Lo = 0x1.ef35793c76730p-45;
+    const double small = fma(ed, kLn2Lo, tb.lo[i]);
+    const double q = fma(t * t, p, small);
+    const double A = fma(ed, kLn2Hi, rl.y);  // exact: both are multiples of 2^-42
+    return A + (t + q);
+}
+
+__device__ __forceinline__ double rsqrt_seed(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+
+__device__ __forceinline__ double rcp_seed(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+
+// 1/sqrt(x): y0 (~2^-23) then y = y0 (1 + e/2 + 3e^2/8), e = 1 - x y0^2  (error ~e^3)
+__device__ __forceinline__ double fast_rsqrt(double x) {
+    const double y = rsqrt_seed(x);
+    const double h = x * y;
+    const double e = fma(-h, y, 1.0);
+    const double c = e * fma(e, 0.375, 0.5);
+    return fma(y, c, y);
+}
+
+// 1/x: y0 then y = y0 (1 + e + e^2), e = 1 - x y0  (error ~e^3)
+__device__ __forceinline__ double fast_rcp(double x) {
+    const double y = rcp_seed(x);
+    const double e = fma(-x, y, 1.0);
+    return fma(y, fma(e, e, e), y);
+}
+
+}  // namespace csfs_b200

@@ -8,22 +8,71 @@
 //   * CTAs pull items from an atomic queue (dynamic, like the reference's
 //     schedule(dynamic,4)); every output slot is owned by exactly one item and summed in
 //     a fixed order, so results are deterministic;
-//   * source points + weights stream through shared memory in SoA chunks (coalesced
-//     global loads, broadcast reads in the inner loop); targets stay in registers;
+//   * source points + weights stream through shared memory in chunks ({x,y},{z,w} pairs:
+//     two broadcast LDS.128 per source per thread); each thread keeps TPT targets in
+//     registers, so every shared-memory source is reused TPT times and the TPT
+//     evaluations are independent FP64 chains (ILP for the DFMA pipe);
 //   * small target sets (49/64/81/121) are packed G groups per CTA that split the source
 //     range and are combined in a fixed order at the end.
 // This is FP64-pipe bound: the inner loop is the kernel functor.
 #include <algorithm>
+#include <cmath>
 
 #include "engine.hpp"
 #include "kernels_dev.cuh"
 
 namespace csfs_b200 {
 
+// tab[i] = {r_i, L_hi_i}, tab[kLogTab + i] = {L_lo_i, 0}: r_i = 1/(1 + (i + 1/2)/256),
+// except r_0 = 1 (m in [1, 1+2^-8)) and r_255 = 1/2 (m in [2-2^-8, 2)), where m r - 1 is
+// exact; -ln r_i = L_hi + L_lo with L_hi on the 2^-42 grid (exact sums with e*ln2_hi),
+// from long-double logl (64-bit mantissa) so L_lo is good to ~1e-19.  The r = 1/2 entry
+// uses exactly the split of ln 2 the device code uses, so e*ln2 + L cancels exactly.
+void make_log_table(double2* tab) {
+    for (int i = 0; i < kLogTab; ++i) {
+        double r = 1.0 / (1.0 + (i + 0.5) / kLogTab);
+        if (i == 0) r = 1.0;
+        if (i == kLogTab - 1) r = 0.5;
+        const long double L = -logl((long double)r);
+        double hi = double(nearbyintl(L * 0x1p42L) / 0x1p42L);
+        double lo = double(L - (long double)hi);
+        if (i == 0) hi = lo = 0.0;
+        if (i == kLogTab - 1) {
+            hi = 0x1.62e42fefa3800p-1;  // fastmath.cuh kLn2Hi / kLn2Lo
+            lo = 0x1.ef35793c76730p-45;
+        }
+        tab[i] = make_double2(r, hi);
+        tab[kLogTab + i] = make_double2(lo, 0.0);
+    }
+}
+
 namespace {
 
-constexpr int kIB = 256;   // threads per CTA
-constexpr int kICH = 256;  // source points per shared-memory chunk
+// Copies the global log table into shared memory; caller syncs before use.
+__device__ __forceinline__ LogTable stage_log_table(double2* s_rl, double* s_lo, const double2* g) {
+    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) {
+        s_rl[i] = g[i];
+        s_lo[i] = g[kLogTab + i].x;
+    }
+    return LogTable{s_rl, s_lo};
+}
+
+#ifndef CSFS_IB
+#define CSFS_IB 256
+#endif
+#ifndef CSFS_TPT
+#define CSFS_TPT 2
+#endif
+#ifndef CSFS_MINB
+#define CSFS_MINB 2
+#endif
+#ifndef CSFS_UNROLL
+#define CSFS_UNROLL 2
+#endif
+constexpr int kIB = CSFS_IB;    // threads per CTA
+constexpr int kTPT = CSFS_TPT;  // targets per thread
+constexpr int kICH = 256;       // source points per shared-memory chunk
+constexpr int kUnroll = CSFS_UNROLL;
 
 struct InteractParams {
     const int4* item;
@@ -38,15 +87,19 @@ struct InteractParams {
     double* out_q;  // proxy potentials (ncl_t x npp x dim)
     const int* anchor;  // per item owner key (nullptr: every item is ours)
     long long own_b, own_e;
+    const double2* log_tab;  // kLogTab entries
 };
 
 template <class Op>
-__global__ void __launch_bounds__(kIB) k_interact(InteractParams P, Op op) {
+__global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, Op op) {
     constexpr int D = Op::dim;
-    __shared__ double sx[kICH], sy[kICH], sz[kICH], sw[kICH];
-    __shared__ double red[kIB * D];
+    __shared__ double2 sxy[kICH], szw[kICH];
+    __shared__ double red[kIB * kTPT * D];
+    __shared__ double2 tab_rl[kLogTab];
+    __shared__ double tab_lo[kLogTab];
     __shared__ int item_sh;
     const int tid = threadIdx.x;
+    const LogTable tab = stage_log_table(tab_rl, tab_lo, P.log_tab);  // synced by the loop's first barrier
     for (;;) {
         if (tid == 0) item_sh = atomicAdd(P.counter, 1);
         __syncthreads();
@@ -60,30 +113,44 @@ __global__ void __launch_bounds__(kIB) k_interact(InteractParams P, Op op) {
         const int4 d = P.item[it];
         const bool tproxy = d.y < 0;
         const int tlen = tproxy ? -d.y : d.y;
-        const int gs = min(kIB, (tlen + 31) & ~31);
+        // group size: threads that together hold the (up to) kIB*kTPT targets of one pass
+        const int per = (tlen + kTPT - 1) / kTPT;
+        const int gs = min(kIB, (per + 31) & ~31);
         const int G = kIB / gs;
         const int g = tid / gs, r = tid - g * gs;
         const double* TX = tproxy ? P.tqx : P.tpx;
         const double* TY = tproxy ? P.tqy : P.tpy;
         const double* TZ = tproxy ? P.tqz : P.tpz;
         double* OUT = tproxy ? P.out_q : P.out_p;
-        for (int t0 = 0; t0 < tlen; t0 += gs) {
-            const int t = t0 + r;
-            const bool active = g < G && t < tlen;
-            double tx = 0.0, ty = 0.0, tz = 1.0;
-            if (active) {
-                tx = TX[d.x + t];
-                ty = TY[d.x + t];
-                tz = TZ[d.x + t];
-            }
-            double acc[D];
+        for (int t0 = 0; t0 < tlen; t0 += gs * kTPT) {
+            const bool grp = g < G;
+            double tx[kTPT], ty[kTPT], tz[kTPT], acc[kTPT][D];
+            bool act[kTPT];
 #pragma unroll
-            for (int k = 0; k < D; ++k) acc[k] = 0.0;
+            for (int k = 0; k < kTPT; ++k) {
+                const int t = t0 + r + k * gs;
+                act[k] = grp && t < tlen;
+                tx[k] = 0.0;
+                ty[k] = 0.0;
+                tz[k] = 1.0;
+                if (act[k]) {
+                    tx[k] = TX[d.x + t];
+                    ty[k] = TY[d.x + t];
+                    tz[k] = TZ[d.x + t];
+                }
+#pragma unroll
+                for (int c = 0; c < D; ++c) acc[k][c] = 0.0;
+            }
+            const bool any = act[0];  // slot 0 is filled first
             int fill = 0;
             auto compute = [&](int n) {
-                if (active) {
-#pragma unroll 2
-                    for (int j = g; j < n; j += G) op(tx, ty, tz, sx[j], sy[j], sz[j], sw[j], acc);
+                if (any) {
+#pragma unroll kUnroll
+                    for (int j = g; j < n; j += G) {
+                        const double2 a = sxy[j], b = szw[j];
+#pragma unroll
+                        for (int k = 0; k < kTPT; ++k) op(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, acc[k], tab);
+                    }
                 }
             };
             for (int e = d.z; e < d.w; ++e) {
@@ -99,10 +166,8 @@ __global__ void __launch_bounds__(kIB) k_interact(InteractParams P, Op op) {
                     const int take = min(len - pos, kICH - fill);
                     for (int j = tid; j < take; j += kIB) {
                         const long long src = (long long)sg.x + pos + j;
-                        sx[fill + j] = X[src];
-                        sy[fill + j] = Y[src];
-                        sz[fill + j] = Z[src];
-                        sw[fill + j] = W[src];
+                        sxy[fill + j] = make_double2(X[src], Y[src]);
+                        szw[fill + j] = make_double2(Z[src], W[src]);
                     }
                     fill += take;
                     pos += take;
@@ -120,21 +185,28 @@ __global__ void __launch_bounds__(kIB) k_interact(InteractParams P, Op op) {
                 __syncthreads();
             }
             if (G > 1) {
-                if (active)
 #pragma unroll
-                    for (int k = 0; k < D; ++k) red[(g * gs + r) * D + k] = acc[k];
+                for (int k = 0; k < kTPT; ++k)
+                    if (act[k])
+#pragma unroll
+                        for (int c = 0; c < D; ++c) red[((g * gs + r) * kTPT + k) * D + c] = acc[k][c];
                 __syncthreads();
-                if (g == 0 && t < tlen) {
+                if (g == 0)
                     for (int h = 1; h < G; ++h)
 #pragma unroll
-                        for (int k = 0; k < D; ++k) acc[k] += red[(h * gs + r) * D + k];
-                }
+                        for (int k = 0; k < kTPT; ++k)
+                            if (act[k])
+#pragma unroll
+                                for (int c = 0; c < D; ++c) acc[k][c] += red[((h * gs + r) * kTPT + k) * D + c];
                 __syncthreads();
             }
-            if (g == 0 && t < tlen) {
+            if (g == 0) {
                 const double sc = op.scale();
 #pragma unroll
-                for (int k = 0; k < D; ++k) OUT[(long long)(d.x + t) * D + k] = acc[k] * sc;
+                for (int k = 0; k < kTPT; ++k)
+                    if (act[k])
+#pragma unroll
+                        for (int c = 0; c < D; ++c) OUT[(long long)(d.x + t0 + r + k * gs) * D + c] = acc[k][c] * sc;
             }
         }
     }
@@ -151,8 +223,42 @@ __global__ void k_aos_to_soa(const double* __restrict__ xyz, long long n, double
 __global__ void k_direct_items(int n_items, long long nt, int4* item, int nseg) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_items) return;
-    const long long t0 = (long long)i * kIB;
-    item[i] = make_int4(int(t0), int(min((long long)kIB, nt - t0)), 0, nseg);
+    const long long t0 = (long long)i * kIB * kTPT;
+    item[i] = make_int4(int(t0), int(min((long long)kIB * kTPT, nt - t0)), 0, nseg);
+}
+
+// Diagnostics: one functor evaluation per (x_i, y_i) pair, scale applied (= the
+// reference's guarded per-pair value; guarded pairs give 0).
+template <class Op>
+__global__ void k_eval_pairs(Op op, const double* x, const double* y, long long n, double* out,
+                             const double2* log_tab) {
+    __shared__ double2 tab_rl[kLogTab];
+    __shared__ double tab_lo[kLogTab];
+    const LogTable tab = stage_log_table(tab_rl, tab_lo, log_tab);
+    __syncthreads();
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc[3] = {0.0, 0.0, 0.0};
+    op(x[3 * i], x[3 * i + 1], x[3 * i + 2], y[3 * i], y[3 * i + 1], y[3 * i + 2], 1.0, acc, tab);
+    for (int c = 0; c < Op::dim; ++c) out[i * Op::dim + c] = acc[c] * op.scale();
+}
+
+__global__ void k_eval_math(int fn, const double* x, long long n, double* out, const double2* log_tab) {
+    __shared__ double2 tab_rl[kLogTab];
+    __shared__ double tab_lo[kLogTab];
+    const LogTable tab = stage_log_table(tab_rl, tab_lo, log_tab);
+    __syncthreads();
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = x[i];
+    double r = 0.0;
+    switch (fn) {
+        case 0: r = fast_log(v, tab); break;
+        case 1: r = fast_rsqrt(v); break;
+        case 2: r = fast_rcp(v); break;
+        default: r = dilog_dev(v, tab); break;
+    }
+    out[i] = r;
 }
 
 template <class F>
@@ -191,7 +297,7 @@ void launch(const InteractParams& p, const Op& op, cudaStream_t s) {
 }  // namespace
 
 void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, const Items& items,
-              double* phi_near, int* work_counter, cudaStream_t s, Own own) {
+              double* phi_near, int* work_counter, const double2* log_tab, cudaStream_t s, Own own) {
     InteractParams p{};
     p.item = items.item;
     p.n_items = items.n_items;
@@ -217,12 +323,14 @@ void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src,
     p.anchor = everything ? nullptr : items.anchor.p;
     p.own_b = own.b;
     p.own_e = own.e;
+    p.log_tab = log_tab;
     with_op(k, [&](auto op) { launch(p, op, s); });
 }
 
 void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, const double* sxyz,
                      const double* sw, long long ns, double* out, DevBuf<double>& soa,
-                     DevBuf<int4>& items, DevBuf<int2>& segs, int* work_counter, cudaStream_t s) {
+                     DevBuf<int4>& items, DevBuf<int2>& segs, int* work_counter,
+                     const double2* log_tab, cudaStream_t s) {
     if (nt == 0) return;
     soa.grow(size_t(3 * nt + 3 * ns));
     double* tx = soa.p;
@@ -243,7 +351,7 @@ void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, cons
     const int nseg = int(hseg.size());
     segs.grow(std::max(nseg, 1));
     if (nseg) CSFS_CK(cudaMemcpyAsync(segs.p, hseg.data(), nseg * sizeof(int2), cudaMemcpyHostToDevice, s));
-    const int n_items = ceil_div(nt, kIB);
+    const int n_items = ceil_div(nt, kIB * kTPT);
     items.grow(n_items);
     k_direct_items<<<ceil_div(n_items, 128), 128, 0, s>>>(n_items, nt, items, nseg);
     CSFS_LAUNCH_CHECK();
@@ -260,8 +368,24 @@ void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, cons
     p.spz = sz;
     p.spw = sw;
     p.out_p = out;
+    p.log_tab = log_tab;
     with_op(k, [&](auto op) { launch(p, op, s); });
     CSFS_CK(cudaStreamSynchronize(s));  // hseg lifetime
+}
+
+void eval_pairs(const KernelSpec& k, const double* x, const double* y, long long n, double* out,
+                const double2* log_tab, cudaStream_t s) {
+    if (n == 0) return;
+    with_op(k, [&](auto op) {
+        k_eval_pairs<<<ceil_div(n, 128), 128, 0, s>>>(op, x, y, n, out, log_tab);
+        CSFS_LAUNCH_CHECK();
+    });
+}
+
+void eval_math(int fn, const double* x, long long n, double* out, const double2* log_tab, cudaStream_t s) {
+    if (n == 0) return;
+    k_eval_math<<<ceil_div(n, 128), 128, 0, s>>>(fn, x, n, out, log_tab);
+    CSFS_LAUNCH_CHECK();
 }
 
 }  // namespace csfs_b200

@@ -3,18 +3,20 @@
 // and of dilog (kernels.cpp:13-51).
 //
 // Same shape as the reference op (static dim; evaluate one (x, y) pair and accumulate
-// w * K(x, y)), with two B200-specific changes that do not alter the value beyond
-// roundoff:
-//  * the coincidence guard `1 - x.y < 1e-14` is predicated (a safe argument is
-//    evaluated and the weight is zeroed) instead of branched, so a warp never diverges;
-//  * the constant prefactor (-1/4pi, 1/4pi, 3 rho/4pi) is applied once per target by
-//    the caller (`scale`) instead of once per pair.
-// `x.y` and `1 - x.y` are evaluated unfused in the reference's order (dot_ref), which
-// keeps the near-neighbour cancellation identical to the reference's build
-// (contraction alone moves results by up to 1.1e-11).
+// w * K(x, y)), re-derived for the FP64 pipe:
+//  * `x.y` and `1 - x.y` are evaluated unfused in the reference's order (dot_ref), so the
+//    near-neighbour cancellation is identical to the reference's build;
+//  * the coincidence guard `1 - x.y < 1e-14` is predicated (a safe argument is evaluated
+//    and the weight zeroed) instead of branched: no divergence, exact skip semantics;
+//  * the prefactor (-1/4pi, 1/4pi, 3 rho/4pi) is applied once per target (`scale`);
+//  * log / rsqrt / rcp come from fastmath.cuh (13 / 5 / 3 FP64 instructions instead of
+//    libdevice's ~28 / 8+8 / 8), each within a few ulp;
+//  * SAL: 1/gamma = rsqrt(2 omc), s = gamma/2 = omc * rsqrt(2 omc) (halving is exact),
+//    log(s (1 + s)) = log(fma(s, s, s)) — the reference's formula, without sqrt or divide.
 #pragma once
 
 #include "common.cuh"
+#include "fastmath.cuh"
 
 namespace csfs_b200 {
 
@@ -22,10 +24,11 @@ struct OpLaplace {
     static constexpr int dim = 1;
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
-                                               double sz, double sw, double* acc) const {
+                                               double sz, double sw, double* acc,
+                                               const LogTable& tab) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
         const bool ok = !(omc < kCoincidenceTol);
-        const double v = log(ok ? omc : 1.0);
+        const double v = fast_log(ok ? omc : 1.0, tab);
         acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
     }
 };
@@ -53,18 +56,18 @@ __device__ __forceinline__ double li2_bernoulli(double z) {
     return fma(z * w, p, fma(-0.25 * z, z, z));
 }
 
-__device__ __forceinline__ double dilog_dev(double u) {
+__device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
     constexpr double kPi2Over6 = kPi * kPi / 6.0;
     if (u > 0.5) {
         const double y = 1.0 - u;  // exact (Sterbenz)
-        const double lu = log(u);
-        const double ly = log(y);
+        const double lu = fast_log(u, tab);
+        const double ly = fast_log(y, tab);  // y == 0 only when u == 1 (selected away)
         const double r = kPi2Over6 - lu * ly - li2_bernoulli(-lu);
         return (u == 1.0) ? kPi2Over6 : r;
     }
     // z = -log1p(-u) via the compensated form log(t) - ((t - 1) + u)/t, t = 1 - u
     const double t = 1.0 - u;
-    const double z = -(log(t) - ((t - 1.0) + u) / t);
+    const double z = -(fast_log(t, tab) - ((t - 1.0) + u) * fast_rcp(t));
     return li2_bernoulli(z);
 }
 
@@ -72,11 +75,12 @@ struct OpBiharmonic {
     static constexpr int dim = 1;
     __device__ __forceinline__ double scale() const { return kInv4Pi; }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
-                                               double sz, double sw, double* acc) const {
+                                               double sz, double sw, double* acc,
+                                               const LogTable& tab) const {
         const double d = dot_ref(tx, ty, tz, sx, sy, sz);
         const double u0 = __dmul_rn(0.5, __dadd_rn(1.0, d));
         const double u = (u0 < 1.0) ? u0 : 1.0;  // std::min(1.0, u0)
-        acc[0] = fma(sw, dilog_dev(u), acc[0]);
+        acc[0] = fma(sw, dilog_dev(u, tab), acc[0]);
     }
 };
 
@@ -84,13 +88,16 @@ struct OpBiotSavart {
     static constexpr int dim = 3;
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
-                                               double sz, double sw, double* acc) const {
+                                               double sz, double sw, double* acc,
+                                               const LogTable&) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
         const bool ok = !(omc < kCoincidenceTol);
-        const double a = (ok ? sw : 0.0) / (ok ? omc : 1.0);
-        const double cx = ty * sz - tz * sy;
-        const double cy = tz * sx - tx * sz;
-        const double cz = tx * sy - ty * sx;
+        const double a = (ok ? sw : 0.0) * fast_rcp(ok ? omc : 1.0);
+        // cross(x, y) unfused, in the reference's order (geometry.hpp:20-22): for close
+        // pairs the components cancel, and a contracted form would differ from it
+        const double cx = __dsub_rn(__dmul_rn(ty, sz), __dmul_rn(tz, sy));
+        const double cy = __dsub_rn(__dmul_rn(tz, sx), __dmul_rn(tx, sz));
+        const double cz = __dsub_rn(__dmul_rn(tx, sy), __dmul_rn(ty, sx));
         acc[0] = fma(a, cx, acc[0]);
         acc[1] = fma(a, cy, acc[1]);
         acc[2] = fma(a, cz, acc[2]);
@@ -102,13 +109,14 @@ struct OpSal {
     double pref, c1, c2;  // SalOp (summation.cpp:64-68)
     __device__ __forceinline__ double scale() const { return pref; }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
-                                               double sz, double sw, double* acc) const {
-        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = !(omc < kCoincidenceTol);
-        const double g2 = 2.0 * (ok ? omc : 1.0);
-        const double gamma = sqrt(g2);
-        const double s = 0.5 * gamma;
-        const double v = c1 / gamma - c2 * log(s * (1.0 + s));
+                                               double sz, double sw, double* acc,
+                                               const LogTable& tab) const {
+        const double omc0 = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = !(omc0 < kCoincidenceTol);
+        const double omc = ok ? omc0 : 1.0;
+        const double r = fast_rsqrt(omc + omc);  // 1/gamma
+        const double s = omc * r;                 // gamma/2
+        const double v = fma(-c2, fast_log(fma(s, s, s), tab), c1 * r);
         acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
     }
 };

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcsfs_b200.so")
+LIB_PATH = os.environ.get("CSFS_B200_LIB") or os.path.join(_HERE, "libcsfs_b200.so")
 
 OK, INVALID_ARGUMENT, CUDA_ERROR, NCCL_ERROR, OUT_OF_MEMORY = 0, 1, 2, 3, 4
 
@@ -153,6 +153,8 @@ def lib() -> C.CDLL:
         L.csfs_b200_probe_fp64.argtypes = [P, C.POINTER(C.c_double)]
         L.csfs_b200_part_plan.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), C.POINTER(_CConfig), P]
         L.csfs_b200_part_units.argtypes = [P, I, C.POINTER(I), P, P, P]
+        L.csfs_b200_eval_pairs.argtypes = [P, C.POINTER(_CKernel), P, P, S, P]
+        L.csfs_b200_eval_math.argtypes = [P, I, P, S, P]
         L.csfs_b200_part_sizes.argtypes = [P, C.POINTER(S), C.POINTER(S)]
         L.csfs_b200_part_upward.argtypes = [P, C.c_longlong, C.c_longlong, P]
         L.csfs_b200_part_eval.argtypes = [P, C.c_longlong, C.c_longlong, P, P]
@@ -319,6 +321,23 @@ class Engine:
 
     def part_finish(self, phi, out):
         self._check(self._lib.csfs_b200_part_finish(self._h, _dptr(phi), _dptr(out)))
+
+    def eval_pairs(self, kernel: Kernel, x, y) -> np.ndarray:
+        """Device functor values K(x_i, y_i) (guarded pairs -> 0), shape (n, out_dim)."""
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3)
+        y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1, 3)
+        out = np.empty((x.shape[0], kernel.out_dim()))
+        self._check(self._lib.csfs_b200_eval_pairs(self._h, C.byref(_ckernel(kernel)), _ptr(x), _ptr(y),
+                                                   x.shape[0], _ptr(out)))
+        return out
+
+    def eval_math(self, fn: str, x) -> np.ndarray:
+        """Device elementary function (log | rsqrt | rcp | dilog) on host values."""
+        code = {"log": 0, "rsqrt": 1, "rcp": 2, "dilog": 3}[fn]
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty_like(x)
+        self._check(self._lib.csfs_b200_eval_math(self._h, code, _ptr(x), x.size, _ptr(out)))
+        return out
 
     def probe_fp64_tflops(self) -> float:
         v = C.c_double()
