@@ -38,6 +38,7 @@ struct csfs_b200_ctx {
     FmmConfig cfg;
     bool have_state = false;
     int dim = 1;
+    bool use_mutual = true;  // symmetric PP evaluation (CSFS_B200_NO_SYMMETRIC=1 disables)
     // multi-GPU partition state (csfs_b200_part_*)
     bool part_planned = false;
     cudaStream_t part_stream = nullptr;
@@ -133,6 +134,16 @@ int count_internal(const DeviceTree& t) {
     return k;
 }
 
+// Symmetric PP evaluation (targets == sources only): pairs within one partition unit.
+void prepare_mutual(csfs_b200_ctx* c, cudaStream_t s) {
+    c->items.mutual = false;
+    if (!c->shared || !c->use_mutual || c->kspec.out_dim() != 1) return;
+    std::vector<long long> ub, ue;
+    partition_units(c->ttree, ub, ue);
+    build_mutual(c->ttree, c->items, ub, c->sc, s);
+    c->items.mutual = c->items.n_partial > 0;
+}
+
 void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
                const double* sw, size_t ns, const KernelSpec& ks, const FmmConfig& f, double* out,
                csfs_b200_stats* st, cudaStream_t s) {
@@ -159,6 +170,7 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
 
     dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
     build_items(T, S, c->lists, c->items, c->sc, s);
+    prepare_mutual(c, s);
     CSFS_CK(cudaEventRecord(ev[3], s));
 
     const int dim = c->dim;
@@ -192,6 +204,9 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
         st->evals_pc = c->items.pair_evals[1];
         st->evals_cp = c->items.pair_evals[2];
         st->evals_cc = c->items.pair_evals[3];
+        st->evals_executed = c->items.pair_evals[0] + c->items.pair_evals[1] + c->items.pair_evals[2] +
+                             c->items.pair_evals[3] - (c->items.mutual ? c->items.skipped_pairs : 0);
+        st->symmetric_pairs = c->items.mutual ? c->items.n_mutual : 0;
         st->tgt_depth = T.depth_max();
         st->tgt_clusters = T.ncl;
         st->tgt_leaves = T.ncl - count_internal(T);
@@ -260,6 +275,8 @@ int csfs_b200_create(csfs_b200_ctx** out, int device) {
         CSFS_CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
         for (auto& e : c->ev) CSFS_CK(cudaEventCreate(&e));
         CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
+        const char* nosym = std::getenv("CSFS_B200_NO_SYMMETRIC");
+        c->use_mutual = !(nosym && nosym[0] == '1');
         std::vector<double2> tab(2 * kLogTab);
         make_log_table(tab.data());
         c->log_tab.grow(2 * kLogTab);
@@ -471,28 +488,15 @@ int csfs_b200_part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const d
         if (!c->shared) build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s);
         dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
         build_items(T, S, c->lists, c->items, c->sc, s);
+        prepare_mutual(c, s);  // same choice as the single-GPU path: bitwise-equal results
         // partition units: depth-1 subtrees plus unsplit roots, in tree order
         for (int w = 0; w < 2; ++w) {
             const DeviceTree& t = (w == 0 || c->shared) ? T : S;
-            const int nfirst = t.depth_max() >= 1 ? t.level_first[1] + t.level_count[1] : 6;
-            std::vector<int> b(nfirst), e(nfirst), nch(nfirst), dep(nfirst);
-            CSFS_CK(cudaMemcpy(b.data(), t.begin.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
-            CSFS_CK(cudaMemcpy(e.data(), t.end.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
-            CSFS_CK(cudaMemcpy(nch.data(), t.nchild.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
-            CSFS_CK(cudaMemcpy(dep.data(), t.depth.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
-            std::vector<std::pair<long long, long long>> u;
-            for (int i = 0; i < nfirst; ++i)
-                if (e[i] > b[i] && (dep[i] == 1 || nch[i] == 0)) u.push_back({b[i], e[i]});
-            std::sort(u.begin(), u.end());
-            c->unit_b[w].clear();
-            c->unit_e[w].clear();
-            for (auto& p : u) {
-                c->unit_b[w].push_back(p.first);
-                c->unit_e[w].push_back(p.second);
-            }
-            c->unit_cost[w].assign(u.size(), 0.0);
+            partition_units(t, c->unit_b[w], c->unit_e[w]);
+            c->unit_cost[w].assign(c->unit_b[w].size(), 0.0);
             if (w == 1)
-                for (size_t i = 0; i < u.size(); ++i) c->unit_cost[1][i] = double(u[i].second - u[i].first);
+                for (size_t i = 0; i < c->unit_b[1].size(); ++i)
+                    c->unit_cost[1][i] = double(c->unit_e[1][i] - c->unit_b[1][i]);
         }
         {
             const int ni = c->items.n_items;

@@ -126,6 +126,18 @@ struct Items {
     int n_items = 0;
     long long n_entries = 0;
     unsigned long long pair_evals[4] = {0, 0, 0, 0};
+    // symmetric PP (build_mutual): per entry flag/leaf pair; per symmetric pair its
+    // {A begin, |A|, B begin, |B|}, partial offset (A block, then B block), owner anchor;
+    // per leaf the partial blocks k_mutual_reduce adds to it (sorted)
+    DevBuf<int> mflag, manchor, mcnt, moff, mcur;
+    DevBuf<int2> epair, mleaf;
+    DevBuf<int4> mpair;
+    DevBuf<long long> mpoff, mlist, unit_b;
+    DevBuf<double> partial;
+    int n_mutual = 0;
+    long long n_partial = 0;  // doubles
+    unsigned long long skipped_pairs = 0;
+    bool mutual = false;
 };
 
 struct KernelSpec {
@@ -172,9 +184,15 @@ void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, in
                     Scratch& sc, cudaStream_t s);
 void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& lists, Items& items,
                  Scratch& sc, cudaStream_t s);
+// Symmetric PP marking (shared tree only); unit_begins = sorted first particles of the
+// partition units (depth-1 subtrees + unsplit roots).
+void build_mutual(const DeviceTree& tgt, Items& items, const std::vector<long long>& unit_begins, Scratch& sc,
+                  cudaStream_t s);
+// Partition units of a tree: (begin, end) particle ranges in tree order.
+void partition_units(const DeviceTree& t, std::vector<long long>& b, std::vector<long long>& e);
 
 // interact.cu
-void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, const Items& items,
+void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, Items& items,
               double* phi_near, int* work_counter, const double2* log_tab, cudaStream_t s, Own own);
 // all-pairs (direct_sum, summation.cpp:136-161): targets/sources AoS in input order.
 void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, const double* sxyz,

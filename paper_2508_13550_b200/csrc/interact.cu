@@ -87,7 +87,7 @@ struct InteractParams {
     double* out_q;  // proxy potentials (ncl_t x npp x dim)
     const int* anchor;  // per item owner key (nullptr: every item is ours)
     long long own_b, own_e;
-    const double2* log_tab;  // kLogTab entries
+    const double2* log_tab;  // 2 x kLogTab entries (fastmath.cuh)
 };
 
 template <class Op>
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
             for (int e = d.z; e < d.w; ++e) {
                 const int2 sg = P.seg[e];
                 const bool sproxy = sg.y < 0;
-                const int len = sproxy ? -sg.y : sg.y;
+                const int len = sproxy ? -sg.y : sg.y;  // 0: evaluated by the symmetric kernel
                 const double* X = sproxy ? P.sqx : P.spx;
                 const double* Y = sproxy ? P.sqy : P.spy;
                 const double* Z = sproxy ? P.sqz : P.spz;
@@ -209,6 +209,114 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                         for (int c = 0; c < D; ++c) OUT[(long long)(d.x + t0 + r + k * gs) * D + c] = acc[k][c] * sc;
             }
         }
+    }
+}
+
+// ---- symmetric PP (scalar kernels, targets == sources) ------------------------------------
+// One CTA per leaf pair {A, B} listed in both directions (A < B): the |A| x |B| block of
+// K(a, b) is evaluated ONCE and applied to both sides: row sums -> A, column sums -> B
+// (K(b, a) = kSym K(a, b) bit-for-bit).  16 x 16 threads: warp w, lane l -> ti = 2w + l/16,
+// tj = l%16; thread (ti, tj) owns targets a = ti + 16k and sources b = tj + 16m
+// (|A|, |B| <= 256).  Rows reduce over tj with shuffles, columns over ti with one shuffle
+// plus a fixed-order pass over the 8 warps: deterministic, no atomics.  Both partial sums
+// go to `partial` and k_mutual_reduce adds them to phi_near after the list items.
+constexpr int kMT = 16;  // thread grid 16 x 16, up to 16 targets x 16 sources per thread
+
+struct MutualParams {
+    const int4* pair;  // {A begin, |A|, B begin, |B|}
+    const long long* poff;  // partial offset of A's block (B's follows at + |A|)
+    const int* anchor;  // A's begin, or -1: every rank
+    int n_pairs;
+    const double *px, *py, *pz, *pw;  // particles (tree order) + weights
+    double* partial;
+    const double2* log_tab;
+    long long own_b, own_e;
+};
+
+template <class Op>
+__global__ void __launch_bounds__(256, 2) k_mutual(MutualParams P, Op op) {
+    static_assert(Op::dim == 1, "symmetric path is for scalar kernels");
+    __shared__ double4 sa[kMT * kMT], sb[kMT * kMT];
+    __shared__ double colbuf[8][kMT * kMT];
+    __shared__ double2 tab_rl[kLogTab];
+    __shared__ double tab_lo[kLogTab];
+    const int p = blockIdx.x;
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const int ti = 2 * w + (lane >> 4), tj = lane & 15;
+    const LogTable tab = stage_log_table(tab_rl, tab_lo, P.log_tab);
+    const int4 q = P.pair[p];
+    if (P.anchor) {
+        const long long a = P.anchor[p];
+        if (a >= 0 && (a < P.own_b || a >= P.own_e)) return;  // CTA-uniform
+    }
+    for (int i = tid; i < q.y; i += 256)
+        sa[i] = make_double4(P.px[q.x + i], P.py[q.x + i], P.pz[q.x + i], P.pw[q.x + i]);
+    for (int i = tid; i < q.w; i += 256)
+        sb[i] = make_double4(P.px[q.z + i], P.py[q.z + i], P.pz[q.z + i], P.pw[q.z + i]);
+    __syncthreads();
+    const int KA = (q.y + kMT - 1) / kMT, KB = (q.w + kMT - 1) / kMT;  // CTA-uniform
+    double row[kMT];
+#pragma unroll
+    for (int k = 0; k < kMT; ++k) row[k] = 0.0;
+#pragma unroll 1
+    for (int m = 0; m < KB; ++m) {
+        const int jb = tj + kMT * m;
+        const bool bval = jb < q.w;
+        const double4 s = sb[bval ? jb : 0];
+        const double ws = bval ? s.w : 0.0;
+        double col = 0.0;
+#pragma unroll
+        for (int k = 0; k < kMT; ++k) {
+            if (k < KA) {
+                const int ia = ti + kMT * k;
+                const bool aval = ia < q.y;
+                const double4 t = sa[aval ? ia : 0];
+                double K[1];
+                op.value(t.x, t.y, t.z, s.x, s.y, s.z, K, tab);
+                row[k] = fma(ws, K[0], row[k]);
+                col = fma(aval ? t.w : 0.0, K[0], col);
+            }
+        }
+        col += __shfl_xor_sync(0xffffffffu, col, 16);  // the warp's two ti rows
+        if (lane < 16) colbuf[w][jb] = col;            // jb < 256 always
+    }
+    // rows: reduce over the 16 tj lanes
+#pragma unroll
+    for (int k = 0; k < kMT; ++k) {
+        if (k < KA) {
+            double v = row[k];
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            const int ia = ti + kMT * k;
+            if (tj == 0 && ia < q.y) P.partial[P.poff[p] + ia] = v * op.scale();
+        }
+    }
+    __syncthreads();
+    const double f = op.scale() * Op::kSym;
+    for (int j = tid; j < q.w; j += 256) {
+        double v = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) v += colbuf[ww][j];
+        P.partial[P.poff[p] + q.y + j] = v * f;
+    }
+}
+
+// phi_near[x] += every symmetric-pair partial of x's leaf, in ascending partial order.
+// One CTA per cluster; owned leaves only.
+__global__ void k_mutual_reduce(const int* __restrict__ begin, const int* __restrict__ end,
+                                const int* __restrict__ mcnt, const int* __restrict__ moff,
+                                const long long* __restrict__ mlist, const double* __restrict__ partial,
+                                double* phi, long long own_b, long long own_e) {
+    const int X = blockIdx.x;
+    const int n = mcnt[X];
+    if (n == 0) return;
+    const int b = begin[X], e = end[X];
+    if (b < own_b || b >= own_e) return;
+    const long long* l = mlist + moff[X];
+    for (int x = b + threadIdx.x; x < e; x += blockDim.x) {
+        double v = phi[x];
+        for (int a = 0; a < n; ++a) v += partial[l[a] + (x - b)];
+        phi[x] = v;
     }
 }
 
@@ -294,9 +402,18 @@ void launch(const InteractParams& p, const Op& op, cudaStream_t s) {
     CSFS_LAUNCH_CHECK();
 }
 
+template <class Op>
+void launch_mutual(const MutualParams& m, const Op& op, cudaStream_t s) {
+    if constexpr (Op::dim == 1) {
+        if (m.n_pairs == 0) return;
+        k_mutual<Op><<<m.n_pairs, 256, 0, s>>>(m, op);
+        CSFS_LAUNCH_CHECK();
+    }
+}
+
 }  // namespace
 
-void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, const Items& items,
+void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, Items& items,
               double* phi_near, int* work_counter, const double2* log_tab, cudaStream_t s, Own own) {
     InteractParams p{};
     p.item = items.item;
@@ -324,7 +441,31 @@ void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src,
     p.own_b = own.b;
     p.own_e = own.e;
     p.log_tab = log_tab;
-    with_op(k, [&](auto op) { launch(p, op, s); });
+    MutualParams m{};
+    if (items.mutual) {
+        items.partial.grow(size_t(std::max<long long>(items.n_partial, 1)));
+        m.pair = items.mpair;
+        m.poff = items.mpoff;
+        m.anchor = everything ? nullptr : items.manchor.p;
+        m.n_pairs = items.n_mutual;
+        m.px = src.px;
+        m.py = src.py;
+        m.pz = src.pz;
+        m.pw = src.w;
+        m.partial = items.partial;
+        m.log_tab = log_tab;
+        m.own_b = own.b;
+        m.own_e = own.e;
+    }
+    with_op(k, [&](auto op) {
+        if (items.mutual) launch_mutual(m, op, s);
+        launch(p, op, s);
+    });
+    if (items.mutual) {
+        k_mutual_reduce<<<tgt.ncl, 128, 0, s>>>(tgt.begin, tgt.end, items.mcnt, items.moff, items.mlist,
+                                                items.partial, phi_near, own.b, own.e);
+        CSFS_LAUNCH_CHECK();
+    }
 }
 
 void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, const double* sxyz,

@@ -20,9 +20,21 @@
 
 namespace csfs_b200 {
 
+// Each op also provides value(): the unscaled, guarded K(t, s) (0 where the guard skips),
+// used by the symmetric PP path, which applies one evaluation to both the target's row
+// and the source's column; kSym: K(s, t) = kSym * K(t, s) (exactly: the unfused dot and
+// cross products commute bit-for-bit).
 struct OpLaplace {
     static constexpr int dim = 1;
+    static constexpr double kSym = 1.0;
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
+    __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
+                                          double* K, const LogTable& tab) const {
+        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = !(omc < kCoincidenceTol);
+        const double v = fast_log(ok ? omc : 1.0, tab);
+        K[0] = ok ? v : 0.0;
+    }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,
                                                const LogTable& tab) const {
@@ -73,7 +85,14 @@ __device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
 
 struct OpBiharmonic {
     static constexpr int dim = 1;
+    static constexpr double kSym = 1.0;
     __device__ __forceinline__ double scale() const { return kInv4Pi; }
+    __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
+                                          double* K, const LogTable& tab) const {
+        const double d = dot_ref(tx, ty, tz, sx, sy, sz);
+        const double u0 = __dmul_rn(0.5, __dadd_rn(1.0, d));
+        K[0] = dilog_dev((u0 < 1.0) ? u0 : 1.0, tab);
+    }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,
                                                const LogTable& tab) const {
@@ -86,7 +105,17 @@ struct OpBiharmonic {
 
 struct OpBiotSavart {
     static constexpr int dim = 3;
+    static constexpr double kSym = -1.0;  // cross(s, t) = -cross(t, s), 1 - s.t = 1 - t.s
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
+    __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
+                                          double* K, const LogTable&) const {
+        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = !(omc < kCoincidenceTol);
+        const double a = ok ? fast_rcp(ok ? omc : 1.0) : 0.0;
+        K[0] = a * __dsub_rn(__dmul_rn(ty, sz), __dmul_rn(tz, sy));
+        K[1] = a * __dsub_rn(__dmul_rn(tz, sx), __dmul_rn(tx, sz));
+        K[2] = a * __dsub_rn(__dmul_rn(tx, sy), __dmul_rn(ty, sx));
+    }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,
                                                const LogTable&) const {
@@ -106,8 +135,19 @@ struct OpBiotSavart {
 
 struct OpSal {
     static constexpr int dim = 1;
+    static constexpr double kSym = 1.0;
     double pref, c1, c2;  // SalOp (summation.cpp:64-68)
     __device__ __forceinline__ double scale() const { return pref; }
+    __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
+                                          double* K, const LogTable& tab) const {
+        const double omc0 = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = !(omc0 < kCoincidenceTol);
+        const double omc = ok ? omc0 : 1.0;
+        const double r = fast_rsqrt(omc + omc);
+        const double s = omc * r;
+        const double v = fma(-c2, fast_log(fma(s, s, s), tab), c1 * r);
+        K[0] = ok ? v : 0.0;
+    }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,
                                                const LogTable& tab) const {

@@ -115,7 +115,199 @@ __global__ void k_items(int n_items, int ncl_t, const int* __restrict__ keys,
     cost[i] = double(tl) * double(src_pts);
 }
 
+__device__ __forceinline__ int unit_of(const long long* ub, int nu, long long b) {
+    int lo = 0, hi = nu;  // last unit with begin <= b
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (ub[mid] <= b) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Symmetric PP (targets == sources, scalar kernels): K(t, s) = kSym K(s, t) bit-for-bit,
+// so a PP pair of leaves {A, B} listed in BOTH directions is evaluated once by the tile
+// kernel k_mutual (both segments are dropped from the list items).  Only pairs inside one
+// partition unit (depth-1 subtree) with |A|, |B| <= 256 qualify, so the choice — and the
+// summation order — is the same for every rank count.
+__global__ void k_mutual_mark(int n_items, int ncl_t, const int* __restrict__ keys,
+                              const int* __restrict__ cnt, const int* __restrict__ off,
+                              const long long* __restrict__ code, int2* seg, int* mflag, int2* epair,
+                              const long long* __restrict__ unit_b, int n_units, const TreeView T,
+                              unsigned long long* saved) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long sv = 0;
+    if (i < n_items) {
+        const int key = keys[i];
+        const int b = off[key], n = cnt[key];
+        for (int a = 0; a < n; ++a) mflag[b + a] = 0;
+        const int t = key;
+        const int nt = key < ncl_t ? T.end[t] - T.begin[t] : 0;
+        if (key < ncl_t && T.depth[t] >= 1 && nt <= 256) {
+            const int ut = unit_of(unit_b, n_units, T.begin[t]);
+            for (int a = 0; a < n; ++a) {
+                const long long c = code[b + a];
+                if ((c >> 32) != 0) break;  // sorted: PP entries come first
+                const int s = int(c & 0xffffffffll);
+                const int ns = T.end[s] - T.begin[s];
+                if (s == t || ns > 256 || T.depth[s] < 1 || unit_of(unit_b, n_units, T.begin[s]) != ut) continue;
+                int lo = off[s], hi = off[s] + cnt[s];  // is (s, t) a PP entry too?
+                const long long want = (long long)(unsigned)t;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (code[mid] < want) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo < off[s] + cnt[s] && code[lo] == want) {
+                    seg[b + a].y = 0;  // both directions leave the list items
+                    if (t < s) {
+                        mflag[b + a] = 1;
+                        epair[b + a] = make_int2(t, s);
+                        sv += (unsigned long long)ns * nt;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, d);
+    if ((threadIdx.x & 31) == 0 && sv) atomicAdd(saved, sv);
+}
+
+__global__ void k_mutual_count(int n_pairs, const int4* __restrict__ pair, const int* __restrict__ leaf_of_begin_unused,
+                               int* mcnt, const int2* __restrict__ pl) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_pairs) return;
+    atomicAdd(&mcnt[pl[p].x], 1);
+    atomicAdd(&mcnt[pl[p].y], 1);
+}
+
+__global__ void k_mutual_fill(int n_pairs, const int4* __restrict__ pair, const long long* __restrict__ poff,
+                              const int2* __restrict__ pl, const int* __restrict__ moff, int* mcur, long long* mlist) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_pairs) return;
+    const int A = pl[p].x, B = pl[p].y;
+    mlist[moff[A] + atomicAdd(&mcur[A], 1)] = poff[p];
+    mlist[moff[B] + atomicAdd(&mcur[B], 1)] = poff[p] + pair[p].y;
+}
+
+__global__ void k_mutual_sort(int ncl, const int* __restrict__ mcnt, const int* __restrict__ moff, long long* mlist) {
+    const int X = blockIdx.x * blockDim.x + threadIdx.x;
+    if (X >= ncl) return;
+    long long* l = mlist + moff[X];
+    for (int a = 1; a < mcnt[X]; ++a) {
+        const long long v = l[a];
+        int j = a - 1;
+        while (j >= 0 && l[j] > v) {
+            l[j + 1] = l[j];
+            --j;
+        }
+        l[j + 1] = v;
+    }
+}
+
 }  // namespace
+
+void partition_units(const DeviceTree& t, std::vector<long long>& ub, std::vector<long long>& ue) {
+    const int nfirst = t.depth_max() >= 1 ? t.level_first[1] + t.level_count[1] : 6;
+    std::vector<int> b(nfirst), e(nfirst), nch(nfirst), dep(nfirst);
+    CSFS_CK(cudaMemcpy(b.data(), t.begin.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
+    CSFS_CK(cudaMemcpy(e.data(), t.end.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
+    CSFS_CK(cudaMemcpy(nch.data(), t.nchild.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
+    CSFS_CK(cudaMemcpy(dep.data(), t.depth.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<std::pair<long long, long long>> u;
+    for (int i = 0; i < nfirst; ++i)
+        if (e[i] > b[i] && (dep[i] == 1 || nch[i] == 0)) u.push_back({b[i], e[i]});
+    std::sort(u.begin(), u.end());
+    ub.clear();
+    ue.clear();
+    for (auto& p : u) {
+        ub.push_back(p.first);
+        ue.push_back(p.second);
+    }
+}
+
+void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>& unit_begins, Scratch& sc,
+                  cudaStream_t s) {
+    const TreeView T = tgt.view();
+    const int ncl = tgt.ncl;
+    const long long ne = std::max<long long>(it.n_entries, 1);
+    it.mflag.grow(ne);
+    it.epair.grow(ne);
+    it.mcnt.grow(ncl);
+    it.moff.grow(ncl);
+    it.mcur.grow(ncl);
+    it.unit_b.grow(std::max<size_t>(unit_begins.size(), 1));
+    it.n_mutual = 0;
+    it.n_partial = 0;
+    it.skipped_pairs = 0;
+    if (it.n_items == 0) return;
+    CSFS_CK(cudaMemcpyAsync(it.unit_b.p, unit_begins.data(), unit_begins.size() * sizeof(long long),
+                            cudaMemcpyHostToDevice, s));
+    CSFS_CK(cudaMemsetAsync(it.pairs.p + 4, 0, sizeof(unsigned long long), s));
+    CSFS_CK(cudaMemsetAsync(it.mcnt.p, 0, ncl * sizeof(int), s));
+    CSFS_CK(cudaMemsetAsync(it.mcur.p, 0, ncl * sizeof(int), s));
+    const int nb = ceil_div(it.n_items, 128);
+    k_mutual_mark<<<nb, 128, 0, s>>>(it.n_items, ncl, it.keys, it.cnt, it.off, it.code, it.seg, it.mflag, it.epair,
+                                     it.unit_b, int(unit_begins.size()), T, it.pairs.p + 4);
+    CSFS_LAUNCH_CHECK();
+    // pair index and partial offset: 2-counter scan over entries
+    sc.tiles.grow(scan_tile_ints(it.n_entries, 2));
+    {
+        const int* mflag = it.mflag;
+        const int2* ep = it.epair;
+        auto f = [=] __device__(long long e, int* c) {
+            if (mflag[e]) {
+                const int2 q = ep[e];
+                c[0] = 1;
+                c[1] = (T.end[q.x] - T.begin[q.x]) + (T.end[q.y] - T.begin[q.y]);
+            }
+        };
+        auto count_only = [=] __device__(long long, const int*, const int*) {};
+        run_scan<2>(it.n_entries, f, count_only, sc.tiles, sc.grand, s);
+        CSFS_CK(cudaMemcpyAsync(sc.host, sc.grand.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaMemcpyAsync(&it.skipped_pairs, it.pairs.p + 4, sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
+        it.n_mutual = sc.host[0];
+        it.n_partial = sc.host[1];
+        const int np = std::max(it.n_mutual, 1);
+        it.mpair.grow(np);
+        it.mpoff.grow(np);
+        it.manchor.grow(np);
+        it.mleaf.grow(np);
+        it.mlist.grow(2 * size_t(np));
+        int4* pair = it.mpair;
+        long long* poff = it.mpoff;
+        int* manchor = it.manchor;
+        int2* leaf = it.mleaf;
+        auto e = [=] __device__(long long i, const int* c, const int* pre) {
+            if (!c[0]) return;
+            const int2 q = ep[i];
+            pair[pre[0]] = make_int4(T.begin[q.x], T.end[q.x] - T.begin[q.x], T.begin[q.y], T.end[q.y] - T.begin[q.y]);
+            poff[pre[0]] = pre[1];
+            manchor[pre[0]] = T.begin[q.x];
+            leaf[pre[0]] = q;
+        };
+        if (it.n_mutual) run_scan<2>(it.n_entries, f, e, sc.tiles, sc.grand, s);
+    }
+    if (it.n_mutual == 0) return;
+    const int pb = ceil_div(it.n_mutual, 256);
+    k_mutual_count<<<pb, 256, 0, s>>>(it.n_mutual, it.mpair, nullptr, it.mcnt, it.mleaf);
+    CSFS_LAUNCH_CHECK();
+    {
+        const int* mcnt = it.mcnt;
+        int* moff = it.moff;
+        sc.tiles.grow(scan_tile_ints(ncl, 1));
+        auto f = [=] __device__(long long i, int* c) { c[0] = mcnt[i]; };
+        auto e = [=] __device__(long long i, const int* c, const int* pre) { moff[i] = pre[0]; };
+        run_scan<1>(ncl, f, e, sc.tiles, sc.grand, s);
+    }
+    k_mutual_fill<<<pb, 256, 0, s>>>(it.n_mutual, it.mpair, it.mpoff, it.mleaf, it.moff, it.mcur, it.mlist);
+    CSFS_LAUNCH_CHECK();
+    k_mutual_sort<<<ceil_div(ncl, 128), 128, 0, s>>>(ncl, it.mcnt, it.moff, it.mlist);
+    CSFS_LAUNCH_CHECK();
+}
 
 void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, int n0, Lists& L,
                     Scratch& sc, cudaStream_t s) {
@@ -187,7 +379,7 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, I
     it.off.grow(nkeys);
     it.cur.grow(nkeys);
     it.keys.grow(nkeys);
-    it.pairs.grow(4);
+    it.pairs.grow(8);
     CSFS_CK(cudaMemsetAsync(it.cnt.p, 0, nkeys * sizeof(int), s));
     CSFS_CK(cudaMemsetAsync(it.cur.p, 0, nkeys * sizeof(int), s));
     CSFS_CK(cudaMemsetAsync(it.pairs.p, 0, 4 * sizeof(unsigned long long), s));

@@ -99,7 +99,8 @@ class SumStats(C.Structure):  # summation.hpp:44-53 + B200 extras
                 ("tgt_depth", C.c_int), ("tgt_clusters", C.c_int), ("tgt_leaves", C.c_int),
                 ("t_lists", C.c_double), ("t_interact", C.c_double),
                 ("evals_pp", C.c_uint64), ("evals_pc", C.c_uint64), ("evals_cp", C.c_uint64),
-                ("evals_cc", C.c_uint64), ("shared_tree", C.c_int)]
+                ("evals_cc", C.c_uint64), ("shared_tree", C.c_int),
+                ("evals_executed", C.c_uint64), ("symmetric_pairs", C.c_int)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

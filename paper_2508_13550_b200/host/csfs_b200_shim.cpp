@@ -1,0 +1,103 @@
+// C++ host shim: the reference's csfs::csfmm_sum / direct_sum signatures
+// (/root/reference/proj/include/csfs/summation.hpp:74-88) implemented on the B200 C-ABI
+// (include/csfs_b200.h).  A maintainer compiles this file against the reference's headers
+// and links libcsfs_b200.so in place of summation.cpp's csfmm_sum.
+// CSFS_B200_SHIM_NAMESPACE lets the tests build it side by side with the reference
+// (tests/cpp/shim_parity.cpp) without a symbol clash.
+#include <stdexcept>
+#include <string>
+
+#include "csfs/summation.hpp"
+#include "csfs_b200.h"
+
+#ifndef CSFS_B200_SHIM_NAMESPACE
+#define CSFS_B200_SHIM_NAMESPACE csfs
+#endif
+
+namespace CSFS_B200_SHIM_NAMESPACE {
+
+using csfs::Kernel;
+using csfs::ParticleSet;
+using csfs::PotentialField;
+using csfs::SumStats;
+using csfs::TraversalConfig;
+
+namespace {
+
+// One context per host thread (the C-ABI contract: calls on a context are serialized).
+csfs_b200_ctx* thread_ctx() {
+    thread_local struct Holder {
+        csfs_b200_ctx* c = nullptr;
+        Holder() {
+            if (csfs_b200_create(&c, 0) != CSFS_B200_OK)
+                throw std::runtime_error("csfs_b200: no usable sm_100 device (there is no CPU fallback)");
+        }
+        ~Holder() { csfs_b200_destroy(c); }
+    } holder;
+    return holder.c;
+}
+
+void check(int rc) {
+    if (rc == CSFS_B200_OK) return;
+    const std::string msg = csfs_b200_last_error(thread_ctx());
+    if (rc == CSFS_B200_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    throw std::runtime_error("csfs_b200: " + msg);
+}
+
+csfs_b200_kernel to_c(const Kernel& k) {
+    return {int(k.kind), k.sal.a1, k.sal.b0, k.sal.b1, k.sal.rho_ratio};
+}
+
+}  // namespace
+
+PotentialField csfmm_sum(const ParticleSet& targets, const ParticleSet& sources, const Kernel& kernel,
+                         const TraversalConfig& config, SumStats* stats) {
+    if (sources.weights.size() != sources.positions.size())
+        throw std::invalid_argument("weight count does not match the tree's particle count");
+    const csfs_b200_kernel k = to_c(kernel);
+    const csfs_b200_config c{config.mac, config.degree, config.n0, config.shrink ? 1 : 0};
+    PotentialField f;
+    f.out_dim = kernel.out_dim();
+    f.values.resize(targets.size() * f.out_dim);
+    csfs_b200_stats st{};
+    const double* tx = targets.positions.empty() ? nullptr : &targets.positions[0].x;
+    const double* sx = sources.positions.empty() ? nullptr : &sources.positions[0].x;
+    check(csfs_b200_csfmm(thread_ctx(), tx, targets.size(), sx, sources.weights.data(), sources.size(), &k,
+                          &c, f.values.data(), &st));
+    if (stats) {
+        *stats = SumStats{};
+        stats->t_tree_build = st.t_tree_build;
+        stats->t_upward = st.t_upward;
+        stats->t_traversal = st.t_traversal;
+        stats->t_downward = st.t_downward;
+        stats->t_total = st.t_total;
+        stats->pp = st.pp;
+        stats->pc = st.pc;
+        stats->cp = st.cp;
+        stats->cc = st.cc;
+        stats->source_tree.depth = st.src_depth;
+        stats->source_tree.cluster_count = st.src_clusters;
+        stats->source_tree.leaf_count = st.src_leaves;
+        stats->target_tree.depth = st.tgt_depth;
+        stats->target_tree.cluster_count = st.tgt_clusters;
+        stats->target_tree.leaf_count = st.tgt_leaves;
+    }
+    return f;
+}
+
+PotentialField direct_sum(const ParticleSet& targets, const ParticleSet& sources, const Kernel& kernel,
+                          int /*threads*/) {
+    if (sources.weights.size() != sources.positions.size())
+        throw std::invalid_argument("source weights and positions differ in length");
+    const csfs_b200_kernel k = to_c(kernel);
+    PotentialField f;
+    f.out_dim = kernel.out_dim();
+    f.values.assign(targets.size() * f.out_dim, 0.0);
+    const double* tx = targets.positions.empty() ? nullptr : &targets.positions[0].x;
+    const double* sx = sources.positions.empty() ? nullptr : &sources.positions[0].x;
+    check(csfs_b200_direct(thread_ctx(), tx, targets.size(), sx, sources.weights.data(), sources.size(), &k,
+                           f.values.data()));
+    return f;
+}
+
+}  // namespace CSFS_B200_SHIM_NAMESPACE
