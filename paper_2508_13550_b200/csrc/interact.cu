@@ -213,19 +213,18 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
 }
 
 // ---- symmetric PP (scalar kernels, targets == sources) ------------------------------------
-// One CTA per leaf pair {A, B} listed in both directions (A < B): the |A| x |B| block of
-// K(a, b) is evaluated ONCE and applied to both sides: row sums -> A, column sums -> B
-// (K(b, a) = kSym K(a, b) bit-for-bit).  16 x 16 threads: warp w, lane l -> ti = 2w + l/16,
-// tj = l%16; thread (ti, tj) owns targets a = ti + 16k and sources b = tj + 16m
-// (|A|, |B| <= 256).  Rows reduce over tj with shuffles, columns over ti with one shuffle
-// plus a fixed-order pass over the 8 warps: deterministic, no atomics.  Both partial sums
-// go to `partial` and k_mutual_reduce adds them to phi_near after the list items.
-constexpr int kMT = 16;  // thread grid 16 x 16, up to 16 targets x 16 sources per thread
-
+// One CTA per leaf pair {A, B} listed in BOTH directions (A < B): every K(a, b) is
+// evaluated ONCE and applied to both sides — row sums to A, column sums to B
+// (K(b, a) = kSym K(a, b) bit-for-bit).  Same register/shared-memory structure as
+// k_interact: A's targets (kTPT per thread) and their weights in registers, B (<= 256
+// points) in shared memory, G thread groups splitting B.  Column partials are reduced per
+// warp with a transposed butterfly over source pairs (5 shuffle steps per 2 sources), then
+// over the group's warps in fixed order: deterministic, no atomics.  Both partial sums go
+// to `partial`; k_mutual_reduce adds them to phi_near after the list items.
 struct MutualParams {
-    const int4* pair;  // {A begin, |A|, B begin, |B|}
+    const int4* pair;       // {A begin, |A|, B begin, |B|}, |A|, |B| <= 256
     const long long* poff;  // partial offset of A's block (B's follows at + |A|)
-    const int* anchor;  // A's begin, or -1: every rank
+    const int* anchor;      // A's begin, or -1: every rank
     int n_pairs;
     const double *px, *py, *pz, *pw;  // particles (tree order) + weights
     double* partial;
@@ -234,70 +233,118 @@ struct MutualParams {
 };
 
 template <class Op>
-__global__ void __launch_bounds__(256, 2) k_mutual(MutualParams P, Op op) {
+__global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op) {
     static_assert(Op::dim == 1, "symmetric path is for scalar kernels");
-    __shared__ double4 sa[kMT * kMT], sb[kMT * kMT];
-    __shared__ double colbuf[8][kMT * kMT];
+    __shared__ double2 sxy[kICH], szw[kICH];
+    __shared__ double colbuf[kIB / 32][kICH];
+    __shared__ double red[kIB * kTPT];
     __shared__ double2 tab_rl[kLogTab];
     __shared__ double tab_lo[kLogTab];
     const int p = blockIdx.x;
-    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-    const int ti = 2 * w + (lane >> 4), tj = lane & 15;
+    const int tid = threadIdx.x, lane = tid & 31;
     const LogTable tab = stage_log_table(tab_rl, tab_lo, P.log_tab);
     const int4 q = P.pair[p];
     if (P.anchor) {
         const long long a = P.anchor[p];
         if (a >= 0 && (a < P.own_b || a >= P.own_e)) return;  // CTA-uniform
     }
-    for (int i = tid; i < q.y; i += 256)
-        sa[i] = make_double4(P.px[q.x + i], P.py[q.x + i], P.pz[q.x + i], P.pw[q.x + i]);
-    for (int i = tid; i < q.w; i += 256)
-        sb[i] = make_double4(P.px[q.z + i], P.py[q.z + i], P.pz[q.z + i], P.pw[q.z + i]);
+    for (int j = tid; j < q.w; j += kIB) {
+        sxy[j] = make_double2(P.px[q.z + j], P.py[q.z + j]);
+        szw[j] = make_double2(P.pz[q.z + j], P.pw[q.z + j]);
+    }
+    const int tlen = q.y, nb = q.w;
+    const int per = (tlen + kTPT - 1) / kTPT;
+    const int gs = min(kIB, (per + 31) & ~31);
+    const int G = kIB / gs;
+    const int g = tid / gs, r = tid - g * gs, wig = r >> 5;
+    const bool grp = g < G;
+    double tx[kTPT], ty[kTPT], tz[kTPT], tw[kTPT], acc[kTPT];
+    bool act[kTPT];
+#pragma unroll
+    for (int k = 0; k < kTPT; ++k) {
+        const int t = r + k * gs;
+        act[k] = grp && t < tlen;
+        tx[k] = 0.0;
+        ty[k] = 0.0;
+        tz[k] = 1.0;
+        tw[k] = 0.0;
+        if (act[k]) {
+            tx[k] = P.px[q.x + t];
+            ty[k] = P.py[q.x + t];
+            tz[k] = P.pz[q.x + t];
+            tw[k] = P.pw[q.x + t];
+        }
+        acc[k] = 0.0;
+    }
     __syncthreads();
-    const int KA = (q.y + kMT - 1) / kMT, KB = (q.w + kMT - 1) / kMT;  // CTA-uniform
-    double row[kMT];
+    if (grp) {
+        // 8 sources (j + m*G, m < 8) per step; their per-thread column partials are reduced
+        // over the warp by a transposed butterfly: 4+2+1+1+1 shuffles for 8 sources
+        constexpr int kB = 8;
+        for (int j = g; j < nb; j += kB * G) {
+            double c[kB];
 #pragma unroll
-    for (int k = 0; k < kMT; ++k) row[k] = 0.0;
-#pragma unroll 1
-    for (int m = 0; m < KB; ++m) {
-        const int jb = tj + kMT * m;
-        const bool bval = jb < q.w;
-        const double4 s = sb[bval ? jb : 0];
-        const double ws = bval ? s.w : 0.0;
-        double col = 0.0;
+            for (int m = 0; m < kB; ++m) {
+                c[m] = 0.0;
+                const int jm = j + m * G;
+                if (jm < nb) {  // group-uniform
+                    const double2 a = sxy[jm], b = szw[jm];
 #pragma unroll
-        for (int k = 0; k < kMT; ++k) {
-            if (k < KA) {
-                const int ia = ti + kMT * k;
-                const bool aval = ia < q.y;
-                const double4 t = sa[aval ? ia : 0];
-                double K[1];
-                op.value(t.x, t.y, t.z, s.x, s.y, s.z, K, tab);
-                row[k] = fma(ws, K[0], row[k]);
-                col = fma(aval ? t.w : 0.0, K[0], col);
+                    for (int k = 0; k < kTPT; ++k) {
+                        double K[1];
+                        op.value(tx[k], ty[k], tz[k], a.x, a.y, b.x, K, tab);
+                        acc[k] = fma(b.y, K[0], acc[k]);
+                        c[m] = fma(tw[k], K[0], c[m]);
+                    }
+                }
             }
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+            double v4[4], v2[2];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {  // lanes < 16 keep sources 0..3, >= 16 keep 4..7
+                const double keep = b4 ? c[m + 4] : c[m];
+                const double send = b4 ? c[m] : c[m + 4];
+                v4[m] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                const double keep = b3 ? v4[m + 2] : v4[m];
+                const double send = b3 ? v4[m] : v4[m + 2];
+                v2[m] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            double v = (b2 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? v2[0] : v2[1], 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            const int m = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+            const int jm = j + m * G;
+            if ((lane & 3) == 0 && jm < nb) colbuf[wig][jm] = v;
         }
-        col += __shfl_xor_sync(0xffffffffu, col, 16);  // the warp's two ti rows
-        if (lane < 16) colbuf[w][jb] = col;            // jb < 256 always
     }
-    // rows: reduce over the 16 tj lanes
+    // rows: combine the G groups (fixed order), then write A's block
+    if (G > 1) {
 #pragma unroll
-    for (int k = 0; k < kMT; ++k) {
-        if (k < KA) {
-            double v = row[k];
-#pragma unroll
-            for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            const int ia = ti + kMT * k;
-            if (tj == 0 && ia < q.y) P.partial[P.poff[p] + ia] = v * op.scale();
-        }
+        for (int k = 0; k < kTPT; ++k)
+            if (act[k]) red[(g * gs + r) * kTPT + k] = acc[k];
     }
     __syncthreads();
-    const double f = op.scale() * Op::kSym;
-    for (int j = tid; j < q.w; j += 256) {
-        double v = 0.0;
+    if (G > 1 && g == 0)
+        for (int h = 1; h < G; ++h)
 #pragma unroll
-        for (int ww = 0; ww < 8; ++ww) v += colbuf[ww][j];
-        P.partial[P.poff[p] + q.y + j] = v * f;
+            for (int k = 0; k < kTPT; ++k)
+                if (act[k]) acc[k] += red[(h * gs + r) * kTPT + k];
+    const long long base = P.poff[p];
+    if (g == 0) {
+#pragma unroll
+        for (int k = 0; k < kTPT; ++k)
+            if (act[k]) P.partial[base + r + k * gs] = acc[k] * op.scale();
+    }
+    // columns: source j was handled by group j % G, whose warps wrote colbuf[0..W)[j]
+    const int W = gs >> 5;
+    const double f = op.scale() * Op::kSym;
+    for (int j = tid; j < nb; j += kIB) {
+        double v = 0.0;
+        for (int w = 0; w < W; ++w) v += colbuf[w][j];
+        P.partial[base + tlen + j] = v * f;
     }
 }
 
@@ -406,7 +453,7 @@ template <class Op>
 void launch_mutual(const MutualParams& m, const Op& op, cudaStream_t s) {
     if constexpr (Op::dim == 1) {
         if (m.n_pairs == 0) return;
-        k_mutual<Op><<<m.n_pairs, 256, 0, s>>>(m, op);
+        k_mutual<Op><<<m.n_pairs, kIB, 0, s>>>(m, op);
         CSFS_LAUNCH_CHECK();
     }
 }

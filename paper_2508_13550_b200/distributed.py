@@ -87,7 +87,7 @@ def partitioned_csfmm(engine, tgt_xyz, src_xyz, src_w, kernel, config, out, grou
 
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    if allreduce is None and world > 1:
+    if allreduce is None and dist.is_initialized():
         def allreduce(t):
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     bufs = bufs if bufs is not None else getattr(engine, "_exchange", None) or ExchangeBuffers()
