@@ -99,6 +99,20 @@ CSFS_B200_API int csfs_b200_direct_device(csfs_b200_ctx* ctx, const double* tgt_
                             const double* src_xyz, const double* src_w, size_t ns,
                             const csfs_b200_kernel* kernel, double* out, void* stream);
 
+/* --- barotropic vorticity: one RK4 step (applications.cpp:378-412, remesh off) -------------
+ * Four Biot-Savart CSFMM sums with device-resident stage positions: k_i = u(pos_i, zeta_i),
+ * pos = normalized(x + h k), zeta_i = zeta - 2 Omega h k.z; then x <- normalized(x + du),
+ * zeta -= 2 Omega du.z, du = dt/6 (k1 + 2k2 + 2k3 + k4).  xyz (n x 3) and zeta (n) are
+ * updated in place; areas (n) frozen.  stage_stats: NULL or 4 entries.  dt <= 0 -> code 1
+ * "time step must be positive" (the reference's std::invalid_argument). */
+CSFS_B200_API int csfs_b200_bve_step(csfs_b200_ctx* ctx, double* xyz, double* zeta, const double* areas,
+                                     size_t n, double omega, double dt, const csfs_b200_config* config,
+                                     csfs_b200_stats* stage_stats);
+CSFS_B200_API int csfs_b200_bve_step_device(csfs_b200_ctx* ctx, double* xyz, double* zeta,
+                                            const double* areas, size_t n, double omega, double dt,
+                                            const csfs_b200_config* config, csfs_b200_stats* stage_stats,
+                                            void* stream);
+
 /* --- stepwise state of the LAST csfmm call (parity / inspection) ------------------------
  * which: 0 target tree, 1 source tree.  Cluster ids are the REFERENCE's ids
  * (LIFO expansion order, cluster_tree.cpp:87-140). */

@@ -32,6 +32,7 @@ struct csfs_b200_ctx {
     DevBuf<int4> d_items;
     DevBuf<int2> d_segs;
     DevBuf<double2> log_tab;  // fastmath.cuh table, uploaded once per context
+    DevBuf<double> bve;       // RK4 stage buffers (csfs_b200_bve_step)
     cudaEvent_t ev[8] = {};
     Cheb cheb{};
     KernelSpec kspec;
@@ -460,6 +461,59 @@ int csfs_b200_proxy_weights_export(csfs_b200_ctx* c, double* pw) {
         CSFS_CK(cudaMemcpy(q.data(), s.qw.p, nq * sizeof(double), cudaMemcpyDeviceToHost));
         for (int i = 0; i < s.ncl; ++i)
             std::memcpy(pw + size_t(h.ref[i]) * s.npp, q.data() + size_t(i) * s.npp, s.npp * sizeof(double));
+    });
+}
+
+// --- BVE RK4 step (applications.cpp:378-412, remesh off) ---------------------------------
+
+int csfs_b200_bve_step_device(csfs_b200_ctx* c, double* xyz, double* zeta, const double* areas, size_t n,
+                              double omega, double dt, const csfs_b200_config* cfg,
+                              csfs_b200_stats* stage_stats, void* stream) {
+    return guarded(c, [&] {
+        if (dt <= 0.0) throw InvalidArgument("time step must be positive");
+        const FmmConfig f = to_cfg(cfg);
+        validate(f, n, n);
+        cudaStream_t s = pick(c, stream);
+        KernelSpec ks;
+        ks.kind = 2;  // Biot-Savart (biot_savart_velocity, applications.cpp:181-196)
+        const long long N = (long long)n;
+        c->bve.grow(size_t(N) * 17);
+        double* k[4];  // stage velocities, n x 3 each
+        for (int q = 0; q < 4; ++q) k[q] = c->bve.p + size_t(N) * 3 * q;
+        double* pos = c->bve.p + size_t(N) * 12;  // stage positions
+        double* zs = pos + size_t(N) * 3;         // stage vorticity
+        double* w = zs + N;                       // stage weights zeta * area
+        const double* x0 = xyz;  // xyz and zeta keep the step's initial state until bve_final
+        bve_weights(N, zeta, areas, w, s);
+        const double hs[3] = {0.5 * dt, 0.5 * dt, dt};
+        for (int q = 0; q < 4; ++q) {
+            const double* P = q == 0 ? x0 : pos;
+            run_csfmm(c, P, n, P, w, n, ks, f, k[q], stage_stats ? stage_stats + q : nullptr, s);
+            if (q < 3) bve_advance(N, x0, zeta, k[q], hs[q], omega, areas, pos, zs, w, s);
+        }
+        bve_final(N, xyz, zeta, k[0], k[1], k[2], k[3], dt, omega, s);
+        CSFS_CK(cudaStreamSynchronize(s));
+    });
+}
+
+int csfs_b200_bve_step(csfs_b200_ctx* c, double* xyz, double* zeta, const double* areas, size_t n, double omega,
+                       double dt, const csfs_b200_config* cfg, csfs_b200_stats* stage_stats) {
+    return guarded(c, [&] {
+        if (dt <= 0.0) throw InvalidArgument("time step must be positive");
+        validate(to_cfg(cfg), n, n);
+        cudaStream_t s = c->own;
+        c->h_txyz.grow(n * 3);
+        c->h_w.grow(n);
+        c->h_out.grow(n);
+        CSFS_CK(cudaMemcpyAsync(c->h_txyz.p, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        CSFS_CK(cudaMemcpyAsync(c->h_w.p, zeta, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        CSFS_CK(cudaMemcpyAsync(c->h_out.p, areas, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        const int rc = csfs_b200_bve_step_device(c, c->h_txyz.p, c->h_w.p, c->h_out.p, n, omega, dt, cfg,
+                                                 stage_stats, s);
+        if (rc != CSFS_B200_OK) throw CudaFailure(c->err);
+        CSFS_CK(cudaMemcpyAsync(xyz, c->h_txyz.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaMemcpyAsync(zeta, c->h_w.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
     });
 }
 

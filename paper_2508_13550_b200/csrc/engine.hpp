@@ -206,6 +206,13 @@ void eval_pairs(const KernelSpec& k, const double* x, const double* y, long long
 void eval_math(int fn, const double* x, long long n, double* out, const double2* log_tab, cudaStream_t s);
 void make_log_table(double2* tab);
 
+// bve.cu: RK4 stage arithmetic of bve_step (applications.cpp:378-412)
+void bve_weights(long long n, const double* zeta, const double* area, double* w, cudaStream_t s);
+void bve_advance(long long n, const double* x0, const double* z0, const double* k, double h, double omega,
+                 const double* area, double* pos, double* zeta, double* w, cudaStream_t s);
+void bve_final(long long n, double* x, double* zeta, const double* k1, const double* k2, const double* k3,
+               const double* k4, double dt, double omega, cudaStream_t s);
+
 // passes.cu: out[perm[t]] = phi_tree[t] (multi-GPU finish).
 void scatter_to_input(const DeviceTree& tgt, int dim, const double* phi_tree, double* out, cudaStream_t s);
 

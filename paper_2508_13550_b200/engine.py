@@ -154,6 +154,10 @@ def lib() -> C.CDLL:
         L.csfs_b200_probe_fp64.argtypes = [P, C.POINTER(C.c_double)]
         L.csfs_b200_part_plan.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), C.POINTER(_CConfig), P]
         L.csfs_b200_part_units.argtypes = [P, I, C.POINTER(I), P, P, P]
+        L.csfs_b200_bve_step.argtypes = [P, P, P, P, S, C.c_double, C.c_double, C.POINTER(_CConfig),
+                                         C.POINTER(SumStats)]
+        L.csfs_b200_bve_step_device.argtypes = [P, P, P, P, S, C.c_double, C.c_double, C.POINTER(_CConfig),
+                                                C.POINTER(SumStats), P]
         L.csfs_b200_eval_pairs.argtypes = [P, C.POINTER(_CKernel), P, P, S, P]
         L.csfs_b200_eval_math.argtypes = [P, I, P, S, P]
         L.csfs_b200_part_sizes.argtypes = [P, C.POINTER(S), C.POINTER(S)]
@@ -292,6 +296,26 @@ class Engine:
         bufs = [np.empty((max(counts[k], 0), 2), np.int32) for k in range(4)]
         self._check(self._lib.csfs_b200_lists_export(self._h, counts, *[_ptr(b) for b in bufs]))
         return dict(zip(["pp", "pc", "cp", "cc"], bufs))
+
+    # --- barotropic vorticity RK4 step (applications.cpp:378-412, remesh off) ---------
+    def bve_step(self, xyz: np.ndarray, zeta: np.ndarray, areas: np.ndarray, omega: float, dt: float,
+                 config: TraversalConfig) -> tuple[np.ndarray, np.ndarray, list]:
+        """Returns (new positions, new vorticity, per-stage SumStats); inputs untouched."""
+        x = np.array(xyz, dtype=np.float64, order="C", copy=True)
+        z = np.array(zeta, dtype=np.float64, copy=True)
+        a = np.ascontiguousarray(areas, dtype=np.float64)
+        st = (SumStats * 4)()
+        self._check(self._lib.csfs_b200_bve_step(self._h, _ptr(x), _ptr(z), _ptr(a), x.shape[0], float(omega),
+                                                 float(dt), C.byref(_cconfig(config)), st))
+        return x, z, list(st)
+
+    def bve_step_device(self, xyz, zeta, areas, n: int, omega: float, dt: float, config: TraversalConfig,
+                        stream: int = 0) -> list:
+        st = (SumStats * 4)()
+        self._check(self._lib.csfs_b200_bve_step_device(self._h, _dptr(xyz), _dptr(zeta), _dptr(areas), n,
+                                                        float(omega), float(dt), C.byref(_cconfig(config)), st,
+                                                        C.c_void_p(stream)))
+        return list(st)
 
     # --- multi-GPU partition phases (see distributed.py) ------------------------------
     def part_plan(self, tgt_xyz, nt, src_xyz, src_w, ns, kernel, config, stream=0):
