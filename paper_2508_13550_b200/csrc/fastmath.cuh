@@ -76,4 +76,43 @@ __device__ __forceinline__ double fast_rcp(double x) {
     return fma(y, fma(e, e, e), y);
 }
 
+// bary_basis_1d (interpolation.cpp:26-43) for the per-particle P2M / L2P bases: the same
+// node-coincidence test and summation order, with the np + 1 IEEE divisions replaced by
+// fast reciprocals (<= 2 ulp each; proxy weights/potentials move by ~1e-16 relative).
+// NP > 0: compile-time node count (fully unrolled, `out` stays in registers); 0: c.np.
+template <int NP = 0>
+__device__ __forceinline__ void bary1d_fast(const Cheb& c, double x, double* out) {
+    const int np = NP > 0 ? NP : c.np;
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < (NP > 0 ? NP : kMaxNp); ++k)
+        if (k < np) {
+            const bool h = fabs(x - c.nodes[k]) < kNodeTol;
+            out[k] = h ? 1.0 : 0.0;  // indicator if some node coincides (first one wins below)
+            hit = hit || h;
+        }
+    if (hit) {
+        bool seen = false;  // the reference returns the FIRST coincident node's indicator
+#pragma unroll
+        for (int k = 0; k < (NP > 0 ? NP : kMaxNp); ++k)
+            if (k < np) {
+                if (seen) out[k] = 0.0;
+                seen = seen || out[k] != 0.0;
+            }
+        return;
+    }
+    double denom = 0.0;
+#pragma unroll
+    for (int k = 0; k < (NP > 0 ? NP : kMaxNp); ++k)
+        if (k < np) {
+            const double q = c.weights[k] * fast_rcp(x - c.nodes[k]);
+            out[k] = q;
+            denom += q;
+        }
+    const double inv = fast_rcp(denom);
+#pragma unroll
+    for (int k = 0; k < (NP > 0 ? NP : kMaxNp); ++k)
+        if (k < np) out[k] *= inv;
+}
+
 }  // namespace csfs_b200

@@ -11,6 +11,7 @@
 #include <algorithm>
 
 #include "engine.hpp"
+#include "fastmath.cuh"
 
 namespace csfs_b200 {
 
@@ -49,8 +50,8 @@ __global__ void __launch_bounds__(kPassThreads)
             const int p = base + threadIdx.x;
             double* wl = WL + threadIdx.x * np;
             double* ly = LY + threadIdx.x * np;
-            bary1d(cheb, ref_coord(t.xi[p], xm, xh), wl);
-            bary1d(cheb, ref_coord(t.eta[p], em, eh), ly);
+            bary1d_fast(cheb, ref_coord(t.xi[p], xm, xh), wl);
+            bary1d_fast(cheb, ref_coord(t.eta[p], em, eh), ly);
             const double wt = w[p];
             for (int k = 0; k < np; ++k) wl[k] = __dmul_rn(wt, wl[k]);
         }
@@ -168,36 +169,47 @@ __global__ void __launch_bounds__(kPassThreads)
 }
 
 // L2P (cluster_tree.cpp:241-255) fused with the final scatter to input order:
-// out[perm[t]] = near[t] + sum_k Lx[k1] Ly[k2] P[k].
+// out[perm[t]] = near[t] + sum_k Lx[k1] Ly[k2] P[k].  NP > 0: compile-time (p+1), bases in
+// registers; NP = 0: any degree.
+template <int NP, int D>
 __global__ void __launch_bounds__(kPassThreads)
-    k_l2p(TreeView t, Cheb cheb, int dim, const double* __restrict__ qphi,
-          const double* __restrict__ near, double* __restrict__ out, Own own, bool out_perm) {
+    k_l2p(TreeView t, Cheb cheb, const double* __restrict__ qphi, const double* __restrict__ near,
+          double* __restrict__ out, Own own, bool out_perm) {
     extern __shared__ double sm[];
     const int c = blockIdx.x;
     if (t.nchild[c] > 0) return;
     const int b = t.begin[c], e = t.end[c];
     if (b == e || b < own.b || b >= own.e) return;
-    const int np = cheb.np, npp = np * np;
-    for (int o = threadIdx.x; o < npp * dim; o += kPassThreads) sm[o] = qphi[(long long)c * npp * dim + o];
+    const int np = NP > 0 ? NP : cheb.np, npp = np * np;
+    for (int o = threadIdx.x; o < npp * D; o += kPassThreads) sm[o] = qphi[(long long)c * npp * D + o];
     __syncthreads();
     double xm, xh, em, eh;
     mid_half(t.xi0[c], t.xi1[c], xm, xh);
     mid_half(t.eta0[c], t.eta1[c], em, eh);
+    constexpr int M = NP > 0 ? NP : kMaxNp;
     for (int p = b + threadIdx.x; p < e; p += kPassThreads) {
-        double lx[kMaxNp], ly[kMaxNp];
-        bary1d(cheb, ref_coord(t.xi[p], xm, xh), lx);
-        bary1d(cheb, ref_coord(t.eta[p], em, eh), ly);
-        double f[3] = {0.0, 0.0, 0.0};
-        for (int k1 = 0; k1 < np; ++k1) {
+        double lx[M], ly[M];
+        bary1d_fast<NP>(cheb, ref_coord(t.xi[p], xm, xh), lx);
+        bary1d_fast<NP>(cheb, ref_coord(t.eta[p], em, eh), ly);
+        double f[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) f[d] = 0.0;
+#pragma unroll
+        for (int k1 = 0; k1 < M; ++k1) {
+            if (k1 >= np) break;
             const double a = lx[k1];
-            const double* row = sm + k1 * np * dim;
-            for (int k2 = 0; k2 < np; ++k2) {
+            const double* row = sm + k1 * np * D;
+#pragma unroll
+            for (int k2 = 0; k2 < M; ++k2) {
+                if (k2 >= np) break;
                 const double bb = a * ly[k2];
-                for (int d = 0; d < dim; ++d) f[d] += bb * row[k2 * dim + d];
+#pragma unroll
+                for (int d = 0; d < D; ++d) f[d] = fma(bb, row[k2 * D + d], f[d]);
             }
         }
-        const long long dst = (long long)(out_perm ? t.perm[p] : p) * dim;
-        for (int d = 0; d < dim; ++d) out[dst + d] = near[(long long)p * dim + d] + f[d];
+        const long long dst = (long long)(out_perm ? t.perm[p] : p) * D;
+#pragma unroll
+        for (int d = 0; d < D; ++d) out[dst + d] = near[(long long)p * D + d] + f[d];
     }
 }
 
@@ -250,7 +262,24 @@ void downward_pass(DeviceTree& tgt, const Cheb& cheb, int dim, const double* phi
         CSFS_LAUNCH_CHECK();
     }
     const size_t sm_l2p = size_t(npp) * dim * sizeof(double);
-    k_l2p<<<tgt.ncl, kPassThreads, sm_l2p, s>>>(v, cheb, dim, tgt.qphi, phi_near, out, own, out_perm);
+    auto go = [&](auto kern) {
+        kern<<<tgt.ncl, kPassThreads, sm_l2p, s>>>(v, cheb, tgt.qphi, phi_near, out, own, out_perm);
+    };
+    if (dim == 1) {
+        switch (np) {
+            case 7: go(k_l2p<7, 1>); break;
+            case 9: go(k_l2p<9, 1>); break;
+            case 11: go(k_l2p<11, 1>); break;
+            default: go(k_l2p<0, 1>);
+        }
+    } else {
+        switch (np) {
+            case 7: go(k_l2p<7, 3>); break;
+            case 9: go(k_l2p<9, 3>); break;
+            case 11: go(k_l2p<11, 3>); break;
+            default: go(k_l2p<0, 3>);
+        }
+    }
     CSFS_LAUNCH_CHECK();
 }
 

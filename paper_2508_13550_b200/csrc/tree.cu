@@ -98,40 +98,85 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     return v;
 }
 
+// Segmented min/max over each new cluster's particles.  Particles of a cluster are
+// contiguous, so a warp usually sees one cluster: each thread walks kSegItems strided
+// particles, the warp reduces each step and keeps a running result per cluster, and only
+// flushes it (integer atomics on order-preserving encodings: exact, order independent)
+// when the cluster changes.  Mixed warps (cluster boundaries) fall back to per-lane
+// atomics.  V values per particle; op[v] = 0 min, 1 max.
+constexpr int kSegItems = 8;
+
+template <int V>
+struct SegAcc {
+    int cur = -1;
+    unsigned long long acc[V];
+};
+
+template <int V>
+__device__ __forceinline__ void seg_flush(SegAcc<V>& s, unsigned long long* dst, const int (&op)[V]) {
+    if (s.cur >= 0 && (threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (op[v]) atomicMax(&dst[(long long)s.cur * V + v], s.acc[v]);
+            else atomicMin(&dst[(long long)s.cur * V + v], s.acc[v]);
+        }
+    s.cur = -1;
+}
+
+template <int V>
+__device__ __forceinline__ void seg_step(SegAcc<V>& s, int nd, const unsigned long long (&val)[V],
+                                         unsigned long long* dst, const int (&op)[V]) {
+    const int nd0 = __shfl_sync(0xffffffffu, nd, 0);
+    if (__all_sync(0xffffffffu, nd == nd0)) {
+        if (nd0 < 0) return;
+        unsigned long long r[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) r[v] = op[v] ? warp_max_u64(val[v]) : warp_min_u64(val[v]);
+        if (nd0 != s.cur) {
+            seg_flush<V>(s, dst, op);
+            s.cur = nd0;
+#pragma unroll
+            for (int v = 0; v < V; ++v) s.acc[v] = r[v];
+        } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                s.acc[v] = op[v] ? (r[v] > s.acc[v] ? r[v] : s.acc[v]) : (r[v] < s.acc[v] ? r[v] : s.acc[v]);
+        }
+    } else {
+        seg_flush<V>(s, dst, op);
+        if (nd >= 0)
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                if (op[v]) atomicMax(&dst[(long long)nd * V + v], val[v]);
+                else atomicMin(&dst[(long long)nd * V + v], val[v]);
+            }
+    }
+}
+
 // Shrunk bounds: min/max of xi, eta over each new cluster's particles (:53-61).
 __global__ void k_bounds(long long n, int first, const int* nnew_dev, int cnt_host,
                          const int* __restrict__ node, const double* __restrict__ xi,
                          const double* __restrict__ eta, unsigned long long* bnd) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int cnt = nnew_dev ? *nnew_dev : cnt_host;
-    int nd = -1;
-    unsigned long long a = 0, b = 0;
-    if (i < n) {
-        nd = node[i];
-        if (nd >= first && nd < first + cnt) {
-            a = ord_enc(xi[i]);
-            b = ord_enc(eta[i]);
-        } else {
-            nd = -1;
+    const long long base = (long long)blockIdx.x * blockDim.x * kSegItems + threadIdx.x;
+    constexpr int op[4] = {0, 1, 0, 1};
+    SegAcc<4> s;
+    for (int j = 0; j < kSegItems; ++j) {
+        const long long i = base + (long long)j * blockDim.x;
+        int nd = -1;
+        unsigned long long val[4] = {0, 0, 0, 0};
+        if (i < n) {
+            nd = node[i];
+            if (nd >= first && nd < first + cnt) {
+                val[0] = val[1] = ord_enc(xi[i]);
+                val[2] = val[3] = ord_enc(eta[i]);
+            } else {
+                nd = -1;
+            }
         }
+        seg_step<4>(s, nd, val, bnd, op);
     }
-    const int nd0 = __shfl_sync(0xffffffffu, nd, 0);
-    if (__all_sync(0xffffffffu, nd == nd0)) {
-        if (nd0 < 0) return;
-        const unsigned long long amin = warp_min_u64(a), amax = warp_max_u64(a);
-        const unsigned long long bmin = warp_min_u64(b), bmax = warp_max_u64(b);
-        if ((threadIdx.x & 31) == 0) {
-            atomicMin(&bnd[4 * nd0 + 0], amin);
-            atomicMax(&bnd[4 * nd0 + 1], amax);
-            atomicMin(&bnd[4 * nd0 + 2], bmin);
-            atomicMax(&bnd[4 * nd0 + 3], bmax);
-        }
-    } else if (nd >= 0) {
-        atomicMin(&bnd[4 * nd + 0], a);
-        atomicMax(&bnd[4 * nd + 1], a);
-        atomicMin(&bnd[4 * nd + 2], b);
-        atomicMax(&bnd[4 * nd + 3], b);
-    }
+    seg_flush<4>(s, bnd, op);
 }
 
 // Bounds -> interpolant rectangle, centre (:65-66) and the split decision (:95-96).
@@ -167,36 +212,36 @@ __global__ void k_geom(int first, const int* nnew_dev, int cnt_host, ClusterPtrs
     if (sp) atomicAdd(nsplit, 1);
 }
 
-// Radius = max chordal distance from the centre to the cluster's particles (:67-69).
+// Radius = max chordal distance from the centre to the cluster's particles (:67-69);
+// non-negative doubles order like their bit patterns.
 __global__ void k_radius(long long n, int first, const int* nnew_dev, int cnt_host,
                          const int* __restrict__ node, const double* __restrict__ px,
                          const double* __restrict__ py, const double* __restrict__ pz,
                          const double* __restrict__ cx, const double* __restrict__ cy,
                          const double* __restrict__ cz, double* rad) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int cnt = nnew_dev ? *nnew_dev : cnt_host;
-    int nd = -1;
-    unsigned long long r = 0;
-    if (i < n) {
-        nd = node[i];
-        if (nd >= first && nd < first + cnt) {
-            const double dx = __dsub_rn(cx[nd], px[i]);
-            const double dy = __dsub_rn(cy[nd], py[i]);
-            const double dz = __dsub_rn(cz[nd], pz[i]);
-            r = __double_as_longlong(__dsqrt_rn(dot_ref(dx, dy, dz, dx, dy, dz)));
-        } else {
-            nd = -1;
-        }
-    }
+    const long long base = (long long)blockIdx.x * blockDim.x * kSegItems + threadIdx.x;
+    constexpr int op[1] = {1};
     unsigned long long* radu = reinterpret_cast<unsigned long long*>(rad);
-    const int nd0 = __shfl_sync(0xffffffffu, nd, 0);
-    if (__all_sync(0xffffffffu, nd == nd0)) {
-        if (nd0 < 0) return;
-        const unsigned long long m = warp_max_u64(r);
-        if ((threadIdx.x & 31) == 0) atomicMax(&radu[nd0], m);
-    } else if (nd >= 0) {
-        atomicMax(&radu[nd], r);
+    SegAcc<1> s;
+    for (int j = 0; j < kSegItems; ++j) {
+        const long long i = base + (long long)j * blockDim.x;
+        int nd = -1;
+        unsigned long long val[1] = {0};
+        if (i < n) {
+            nd = node[i];
+            if (nd >= first && nd < first + cnt) {
+                const double dx = __dsub_rn(cx[nd], px[i]);
+                const double dy = __dsub_rn(cy[nd], py[i]);
+                const double dz = __dsub_rn(cz[nd], pz[i]);
+                val[0] = __double_as_longlong(__dsqrt_rn(dot_ref(dx, dy, dz, dx, dy, dz)));
+            } else {
+                nd = -1;
+            }
+        }
+        seg_step<1>(s, nd, val, radu, op);
     }
+    seg_flush<1>(s, radu, op);
 }
 
 // --- splitting (cluster_tree.cpp:87-141) ------------------------------------------------
@@ -323,6 +368,12 @@ __global__ void k_proxy(int ncl, int np, Cheb cheb, const int* __restrict__ face
     qz[g] = z;
 }
 
+__global__ void k_gather(long long n, const int* __restrict__ perm, const double* __restrict__ src,
+                         double* __restrict__ dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm[i]];
+}
+
 __global__ void k_equal(const unsigned long long* a, const unsigned long long* b, long long n,
                         int* diff) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -338,14 +389,15 @@ void finish_level(DeviceTree& t, Scratch& sc, int first, const int* nnew_dev, in
     ClusterPtrs c = cluster_ptrs(t);
     const int gb = ceil_div(std::max(cnt_bound, 1), kThreads);
     const int gp = ceil_div(t.n, kThreads);
+    const int gs = ceil_div(t.n, kThreads * kSegItems);
     k_bnd_init<<<gb, kThreads, 0, s>>>(first, nnew_dev, cnt_bound, c);
     CSFS_LAUNCH_CHECK();
-    k_bounds<<<gp, kThreads, 0, s>>>(t.n, first, nnew_dev, cnt_bound, t.node, t.xi, t.eta, t.bnd);
+    k_bounds<<<gs, kThreads, 0, s>>>(t.n, first, nnew_dev, cnt_bound, t.node, t.xi, t.eta, t.bnd);
     CSFS_LAUNCH_CHECK();
     CSFS_CK(cudaMemsetAsync(sc.counters.p + 1, 0, sizeof(int), s));
     k_geom<<<gb, kThreads, 0, s>>>(first, nnew_dev, cnt_bound, c, t.shrink, t.n0, sc.counters.p + 1);
     CSFS_LAUNCH_CHECK();
-    k_radius<<<gp, kThreads, 0, s>>>(t.n, first, nnew_dev, cnt_bound, t.node, t.px, t.py, t.pz,
+    k_radius<<<gs, kThreads, 0, s>>>(t.n, first, nnew_dev, cnt_bound, t.node, t.px, t.py, t.pz,
                                       t.cx, t.cy, t.cz, t.rad);
     CSFS_LAUNCH_CHECK();
 }
@@ -435,7 +487,6 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
     for (DevBuf<int>* b : {&t.perm, &t.node, &t.perm2, &t.node2, &t.rank, &sc.fface}) b->grow(n);
     if (t.has_w) {
         t.w.grow(n);
-        t.w2.grow(n);
     }
     sc.tiles.grow(scan_tile_ints(n, 6));
     sc.grand.grow(8);
@@ -468,8 +519,9 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
             eta[p] = feta[i];
             perm[p] = int(i);
             node[p] = k;
-            if (hw) w[p] = w_in[i];
         };
+        (void)w;
+        (void)hw;
         run_scan<6>(n, f, e, sc.tiles, sc.grand, s);
     }
     k_roots<<<1, 32, 0, s>>>(cluster_ptrs(t), sc.grand);
@@ -523,9 +575,9 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
         k_children<<<1, kScanThreads, 0, s>>>(first, cnt, next_id, c, sc.segP, sc.segE, sc.kid,
                                                sc.koff, sc.counters.p);
         CSFS_LAUNCH_CHECK();
-        PartArrays a{t.px,  t.py,  t.pz,  t.xi,    t.eta,   t.has_w ? t.w.p : nullptr,
-                     t.perm, t.node, t.px2, t.py2, t.pz2,   t.xi2,
-                     t.eta2, t.has_w ? t.w2.p : nullptr, t.perm2, t.node2};
+        // weights are not carried through the levels: gathered once via perm at the end
+        PartArrays a{t.px, t.py, t.pz, t.xi, t.eta, nullptr, t.perm, t.node, t.px2, t.py2, t.pz2, t.xi2,
+                     t.eta2, nullptr, t.perm2, t.node2};
         k_scatter<<<gp, kThreads, 0, s>>>(n, first, cnt, c, a, t.rank, sc.segP, sc.kid, sc.koff);
         CSFS_LAUNCH_CHECK();
         swap_buf(t.px, t.px2);
@@ -535,7 +587,6 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
         swap_buf(t.eta, t.eta2);
         swap_buf(t.perm, t.perm2);
         swap_buf(t.node, t.node2);
-        if (t.has_w) swap_buf(t.w, t.w2);
 
         finish_level(t, sc, next_id, sc.counters.p, 4 * nsplit, s);
         CSFS_CK(cudaMemcpyAsync(sc.host, sc.counters.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -545,6 +596,12 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
         t.ncl += nnew;
         t.level_first.push_back(next_id);
         t.level_count.push_back(nnew);
+    }
+
+    // ---- weights in tree order (permute_weights, summation.cpp:98-104) ---------------------
+    if (t.has_w) {
+        k_gather<<<gp, kThreads, 0, s>>>(n, t.perm, w_in, t.w);
+        CSFS_LAUNCH_CHECK();
     }
 
     // ---- proxy points --------------------------------------------------------------------
