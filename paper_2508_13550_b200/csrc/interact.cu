@@ -73,6 +73,10 @@ constexpr int kIB = CSFS_IB;    // threads per CTA
 constexpr int kTPT = CSFS_TPT;  // targets per thread
 constexpr int kICH = 256;       // source points per shared-memory chunk
 constexpr int kUnroll = CSFS_UNROLL;
+#ifndef CSFS_MTPT
+#define CSFS_MTPT 2
+#endif
+constexpr int kMTPT = CSFS_MTPT;  // targets per thread in the symmetric kernel
 
 struct InteractParams {
     const int4* item;
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
     static_assert(Op::dim == 1, "symmetric path is for scalar kernels");
     __shared__ double2 sxy[kICH], szw[kICH];
     __shared__ double colbuf[kIB / 32][kICH];
-    __shared__ double red[kIB * kTPT];
+    __shared__ double red[kIB * kMTPT];
     __shared__ double2 tab_rl[kLogTab];
     __shared__ double tab_lo[kLogTab];
     const int p = blockIdx.x;
@@ -253,15 +257,15 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
         szw[j] = make_double2(P.pz[q.z + j], P.pw[q.z + j]);
     }
     const int tlen = q.y, nb = q.w;
-    const int per = (tlen + kTPT - 1) / kTPT;
+    const int per = (tlen + kMTPT - 1) / kMTPT;
     const int gs = min(kIB, (per + 31) & ~31);
     const int G = kIB / gs;
     const int g = tid / gs, r = tid - g * gs, wig = r >> 5;
     const bool grp = g < G;
-    double tx[kTPT], ty[kTPT], tz[kTPT], tw[kTPT], acc[kTPT];
-    bool act[kTPT];
+    double tx[kMTPT], ty[kMTPT], tz[kMTPT], tw[kMTPT], acc[kMTPT];
+    bool act[kMTPT];
 #pragma unroll
-    for (int k = 0; k < kTPT; ++k) {
+    for (int k = 0; k < kMTPT; ++k) {
         const int t = r + k * gs;
         act[k] = grp && t < tlen;
         tx[k] = 0.0;
@@ -281,16 +285,16 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
         // 8 sources (j + m*G, m < 8) per step; their per-thread column partials are reduced
         // over the warp by a transposed butterfly: 4+2+1+1+1 shuffles for 8 sources
         constexpr int kB = 8;
-        for (int j = g; j < nb; j += kB * G) {
-            double c[kB];
+        const int full_end = nb - (kB - 1) * G;  // j < full_end: all 8 sources exist
+        auto sources = [&](int j, double (&c)[kB], bool guard) {
 #pragma unroll
             for (int m = 0; m < kB; ++m) {
                 c[m] = 0.0;
                 const int jm = j + m * G;
-                if (jm < nb) {  // group-uniform
+                if (!guard || jm < nb) {  // group-uniform
                     const double2 a = sxy[jm], b = szw[jm];
 #pragma unroll
-                    for (int k = 0; k < kTPT; ++k) {
+                    for (int k = 0; k < kMTPT; ++k) {
                         double K[1];
                         op.value(tx[k], ty[k], tz[k], a.x, a.y, b.x, K, tab);
                         acc[k] = fma(b.y, K[0], acc[k]);
@@ -298,6 +302,11 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
                     }
                 }
             }
+        };
+        for (int j = g; j < nb; j += kB * G) {
+            double c[kB];
+            if (j < full_end) sources(j, c, false);
+            else sources(j, c, true);
             const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
             double v4[4], v2[2];
 #pragma unroll
@@ -323,19 +332,19 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
     // rows: combine the G groups (fixed order), then write A's block
     if (G > 1) {
 #pragma unroll
-        for (int k = 0; k < kTPT; ++k)
-            if (act[k]) red[(g * gs + r) * kTPT + k] = acc[k];
+        for (int k = 0; k < kMTPT; ++k)
+            if (act[k]) red[(g * gs + r) * kMTPT + k] = acc[k];
     }
     __syncthreads();
     if (G > 1 && g == 0)
         for (int h = 1; h < G; ++h)
 #pragma unroll
-            for (int k = 0; k < kTPT; ++k)
-                if (act[k]) acc[k] += red[(h * gs + r) * kTPT + k];
+            for (int k = 0; k < kMTPT; ++k)
+                if (act[k]) acc[k] += red[(h * gs + r) * kMTPT + k];
     const long long base = P.poff[p];
     if (g == 0) {
 #pragma unroll
-        for (int k = 0; k < kTPT; ++k)
+        for (int k = 0; k < kMTPT; ++k)
             if (act[k]) P.partial[base + r + k * gs] = acc[k] * op.scale();
     }
     // columns: source j was handled by group j % G, whose warps wrote colbuf[0..W)[j]
