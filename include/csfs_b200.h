@@ -92,6 +92,18 @@ CSFS_B200_API int csfs_b200_csfmm_device(csfs_b200_ctx* ctx, const double* tgt_x
                            const csfs_b200_kernel* kernel, const csfs_b200_config* config,
                            double* out, csfs_b200_stats* stats, void* stream);
 
+/* csfs::cstc_sum (summation.hpp:77-79, summation.cpp:308-381): the cubed-sphere
+ * treecode — per-target traversal of the source tree, point-cluster MAC, PC via proxies
+ * and PP direct; stats->pp / pc count the per-target interactions like the reference. */
+CSFS_B200_API int csfs_b200_cstc(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt,
+                                 const double* src_xyz, const double* src_w, size_t ns,
+                                 const csfs_b200_kernel* kernel, const csfs_b200_config* config,
+                                 double* out, csfs_b200_stats* stats);
+CSFS_B200_API int csfs_b200_cstc_device(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt,
+                                        const double* src_xyz, const double* src_w, size_t ns,
+                                        const csfs_b200_kernel* kernel, const csfs_b200_config* config,
+                                        double* out, csfs_b200_stats* stats, void* stream);
+
 /* csfs::direct_sum (summation.hpp:74-75, summation.cpp:136-161): O(nt*ns) all pairs. */
 CSFS_B200_API int csfs_b200_direct(csfs_b200_ctx* ctx, const double* tgt_xyz, size_t nt, const double* src_xyz,
                      const double* src_w, size_t ns, const csfs_b200_kernel* kernel, double* out);

@@ -464,6 +464,83 @@ int csfs_b200_proxy_weights_export(csfs_b200_ctx* c, double* pw) {
     });
 }
 
+// --- CSTC treecode (cstc_sum, summation.cpp:308-381) ---------------------------------------
+
+int csfs_b200_cstc_device(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz, const double* sw,
+                          size_t ns, const csfs_b200_kernel* k, const csfs_b200_config* cfg, double* out,
+                          csfs_b200_stats* st, void* stream) {
+    return guarded(c, [&] {
+        const KernelSpec ks = to_spec(k);
+        const FmmConfig f = to_cfg(cfg);
+        // the reference builds only the source tree (its checks: degree, empty set, n0)
+        if (f.degree < 1) throw InvalidArgument("interpolation degree must be positive");
+        if (f.degree > kMaxNp - 1)
+            throw InvalidArgument("interpolation degree above " + std::to_string(kMaxNp - 1) +
+                                  " is not supported by the B200 engine");
+        if (ns == 0) throw InvalidArgument("cannot build a cluster tree from an empty particle set");
+        if (f.resolved_n0() < 1) throw InvalidArgument("maximum leaf size must be at least 1");
+        cudaStream_t s = pick(c, stream);
+        c->have_state = false;
+        c->cheb = make_cheb(f.degree);
+        const int n0 = f.resolved_n0();
+        cudaEvent_t* ev = c->ev;
+        CSFS_CK(cudaEventRecord(ev[0], s));
+        const bool same = (nt == ns) && device_equal(txyz, sxyz, nt * 3 * sizeof(double), c->sc, s);
+        DeviceTree& S = c->stree;
+        build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s);
+        CSFS_CK(cudaEventRecord(ev[1], s));
+        upward_pass(S, c->cheb, s);
+        CSFS_CK(cudaEventRecord(ev[2], s));
+        c->items.pairs.grow(8);
+        cstc_eval(ks, txyz, (long long)nt, same ? S.perm.p : nullptr, S, f.mac, n0, c->log_tab, out,
+                  c->items.pairs.p + 6, s);
+        CSFS_CK(cudaEventRecord(ev[3], s));
+        unsigned long long cnt[2] = {0, 0};
+        CSFS_CK(cudaMemcpyAsync(cnt, c->items.pairs.p + 6, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaEventSynchronize(ev[3]));
+        CSFS_CK(cudaStreamSynchronize(s));
+        if (st) {
+            std::memset(st, 0, sizeof(*st));
+            st->t_tree_build = ev_ms(ev[0], ev[1]) * 1e-3;
+            st->t_upward = ev_ms(ev[1], ev[2]) * 1e-3;
+            st->t_traversal = st->t_interact = ev_ms(ev[2], ev[3]) * 1e-3;
+            st->t_total = ev_ms(ev[0], ev[3]) * 1e-3;
+            st->pp = cnt[0];
+            st->pc = cnt[1];
+            st->src_depth = S.depth_max();
+            st->src_clusters = S.ncl;
+            st->src_leaves = S.ncl - count_internal(S);
+        }
+    });
+}
+
+int csfs_b200_cstc(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz, const double* sw,
+                   size_t ns, const csfs_b200_kernel* k, const csfs_b200_config* cfg, double* out,
+                   csfs_b200_stats* st) {
+    return guarded(c, [&] {
+        const KernelSpec ks = to_spec(k);
+        cudaStream_t s = c->own;
+        const bool same = (txyz == sxyz && nt == ns);
+        c->h_txyz.grow(std::max<size_t>(nt * 3, 1));
+        if (nt) CSFS_CK(cudaMemcpyAsync(c->h_txyz.p, txyz, nt * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        const double* dsrc = c->h_txyz.p;
+        if (!same) {
+            c->h_sxyz.grow(std::max<size_t>(ns * 3, 1));
+            if (ns) CSFS_CK(cudaMemcpyAsync(c->h_sxyz.p, sxyz, ns * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+            dsrc = c->h_sxyz.p;
+        }
+        c->h_w.grow(std::max<size_t>(ns, 1));
+        if (ns) CSFS_CK(cudaMemcpyAsync(c->h_w.p, sw, ns * sizeof(double), cudaMemcpyHostToDevice, s));
+        const size_t nout = nt * size_t(ks.out_dim());
+        c->h_out.grow(std::max<size_t>(nout, 1));
+        const int rc = csfs_b200_cstc_device(c, c->h_txyz.p, nt, dsrc, c->h_w.p, ns, k, cfg, c->h_out.p, st, s);
+        if (rc == CSFS_B200_INVALID_ARGUMENT) throw InvalidArgument(c->err);
+        if (rc != CSFS_B200_OK) throw CudaFailure(c->err);
+        if (nout) CSFS_CK(cudaMemcpyAsync(out, c->h_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
+    });
+}
+
 // --- BVE RK4 step (applications.cpp:378-412, remesh off) ---------------------------------
 
 int csfs_b200_bve_step_device(csfs_b200_ctx* c, double* xyz, double* zeta, const double* areas, size_t n,

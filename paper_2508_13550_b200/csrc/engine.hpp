@@ -206,6 +206,12 @@ void eval_pairs(const KernelSpec& k, const double* x, const double* y, long long
 void eval_math(int fn, const double* x, long long n, double* out, const double2* log_tab, cudaStream_t s);
 void make_log_table(double2* tab);
 
+// cstc.cu: the treecode (cstc_sum, summation.cpp:308-381) over a built + upward-passed
+// source tree; order (nullable) = target processing order; counts[2] = n_pp, n_pc.
+void cstc_eval(const KernelSpec& k, const double* txyz, long long nt, const int* order, const DeviceTree& src,
+               double mac, int n0, const double2* log_tab, double* out, unsigned long long* counts,
+               cudaStream_t s);
+
 // bve.cu: RK4 stage arithmetic of bve_step (applications.cpp:378-412)
 void bve_weights(long long n, const double* zeta, const double* area, double* w, cudaStream_t s);
 void bve_advance(long long n, const double* x0, const double* z0, const double* k, double h, double omega,

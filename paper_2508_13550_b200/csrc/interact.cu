@@ -146,7 +146,6 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                 for (int c = 0; c < D; ++c) acc[k][c] = 0.0;
             }
             const bool any = act[0];  // slot 0 is filled first
-            int fill = 0;
             auto compute = [&](int n) {
                 if (any) {
 #pragma unroll kUnroll
@@ -157,36 +156,46 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                     }
                 }
             };
-            for (int e = d.z; e < d.w; ++e) {
-                const int2 sg = P.seg[e];
-                const bool sproxy = sg.y < 0;
-                const int len = sproxy ? -sg.y : sg.y;  // 0: evaluated by the symmetric kernel
-                const double* X = sproxy ? P.sqx : P.spx;
-                const double* Y = sproxy ? P.sqy : P.spy;
-                const double* Z = sproxy ? P.sqz : P.spz;
-                const double* W = sproxy ? P.sqw : P.spw;
-                int pos = 0;
-                while (pos < len) {
-                    const int take = min(len - pos, kICH - fill);
-                    for (int j = tid; j < take; j += kIB) {
-                        const long long src = (long long)sg.x + pos + j;
-                        sxy[fill + j] = make_double2(X[src], Y[src]);
-                        szw[fill + j] = make_double2(Z[src], W[src]);
+            // Source chunks of kICH points walk the item's segments; the next chunk's global
+            // loads (one point per thread) are issued before the current chunk is evaluated,
+            // so their latency hides behind the FP64 work.
+            static_assert(kICH == kIB, "one source slot per thread");
+            int ce = d.z, cpos = 0;  // cursor into the segment list (CTA-uniform)
+            double rx = 0.0, ry = 0.0, rz = 0.0, rw = 0.0;
+            auto fetch = [&]() {
+                int filled = 0;
+                while (filled < kICH && ce < d.w) {
+                    const int2 sg = P.seg[ce];
+                    const bool sproxy = sg.y < 0;
+                    const int len = sproxy ? -sg.y : sg.y;  // 0: evaluated by the symmetric kernel
+                    const int take = min(len - cpos, kICH - filled);
+                    if (tid >= filled && tid < filled + take) {
+                        const long long src = (long long)sg.x + cpos + (tid - filled);
+                        rx = (sproxy ? P.sqx : P.spx)[src];
+                        ry = (sproxy ? P.sqy : P.spy)[src];
+                        rz = (sproxy ? P.sqz : P.spz)[src];
+                        rw = (sproxy ? P.sqw : P.spw)[src];
                     }
-                    fill += take;
-                    pos += take;
-                    if (fill == kICH) {
-                        __syncthreads();
-                        compute(fill);
-                        __syncthreads();
-                        fill = 0;
+                    filled += take;
+                    cpos += take;
+                    if (cpos == len) {
+                        ++ce;
+                        cpos = 0;
                     }
                 }
-            }
-            if (fill) {
+                return filled;
+            };
+            int n = fetch();
+            while (n > 0) {
+                if (tid < n) {
+                    sxy[tid] = make_double2(rx, ry);
+                    szw[tid] = make_double2(rz, rw);
+                }
                 __syncthreads();
-                compute(fill);
+                const int next = fetch();  // loads in flight during compute
+                compute(n);
                 __syncthreads();
+                n = next;
             }
             if (G > 1) {
 #pragma unroll

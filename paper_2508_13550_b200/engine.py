@@ -144,6 +144,10 @@ def lib() -> C.CDLL:
         L.csfs_b200_csfmm_device.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), C.POINTER(_CConfig),
                                              P, C.POINTER(SumStats), P]
         L.csfs_b200_direct.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), P]
+        L.csfs_b200_cstc.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), C.POINTER(_CConfig), P,
+                                     C.POINTER(SumStats)]
+        L.csfs_b200_cstc_device.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), C.POINTER(_CConfig), P,
+                                            C.POINTER(SumStats), P]
         L.csfs_b200_direct_device.argtypes = [P, P, S, P, P, S, C.POINTER(_CKernel), P, P]
         L.csfs_b200_tree_info.argtypes = [P, I, C.POINTER(I), C.POINTER(I), C.POINTER(S), C.POINTER(I)]
         L.csfs_b200_tree_export.argtypes = [P, I, P, P, P, P]
@@ -250,11 +254,37 @@ class Engine:
                                                C.byref(_ckernel(kernel)), _ptr(out)))
         return PotentialField(kernel.out_dim(), out)
 
+    def cstc_sum(self, targets: ParticleSet, sources: ParticleSet, kernel: Kernel, config: TraversalConfig,
+                 stats: SumStats | None = None) -> PotentialField:
+        """csfs::cstc_sum (summation.cpp:308-381): the treecode."""
+        tx = np.ascontiguousarray(targets.positions, dtype=np.float64)
+        sx = tx if sources.positions is targets.positions else np.ascontiguousarray(sources.positions, dtype=np.float64)
+        sw = np.ascontiguousarray(sources.weights, dtype=np.float64)
+        if sw.shape[0] != sx.shape[0]:
+            raise ValueError("weight count does not match the tree's particle count")
+        out = np.empty(tx.shape[0] * kernel.out_dim())
+        st = stats if stats is not None else SumStats()
+        self._check(self._lib.csfs_b200_cstc(self._h, _ptr(tx), tx.shape[0], _ptr(sx), _ptr(sw), sx.shape[0],
+                                             C.byref(_ckernel(kernel)), C.byref(_cconfig(config)), _ptr(out),
+                                             C.byref(st)))
+        return PotentialField(kernel.out_dim(), out)
+
     def summed_potential(self, targets, sources, kernel, config, stats=None) -> PotentialField:
+        """summation.cpp:423-440: dispatch on config.method."""
         if config.method == Method.Direct:
+            if stats is not None:
+                import time
+
+                t0 = time.perf_counter()
+                f = self.direct_sum(targets, sources, kernel)
+                for k, _ in SumStats._fields_:
+                    setattr(stats, k, type(getattr(stats, k))())
+                stats.t_traversal = stats.t_total = time.perf_counter() - t0
+                stats.pp = targets.size() * sources.size()
+                return f
             return self.direct_sum(targets, sources, kernel)
         if config.method == Method.Cstc:
-            raise NotImplementedError("CSTC (summation.cpp:308-381) is not on the B200 hot path yet")
+            return self.cstc_sum(targets, sources, kernel, config, stats)
         return self.csfmm_sum(targets, sources, kernel, config, stats)
 
     # --- device-resident entry (torch tensors / raw device pointers) --------------------
