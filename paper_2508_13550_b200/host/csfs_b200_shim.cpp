@@ -85,6 +85,35 @@ PotentialField csfmm_sum(const ParticleSet& targets, const ParticleSet& sources,
     return f;
 }
 
+PotentialField cstc_sum(const ParticleSet& targets, const ParticleSet& sources, const Kernel& kernel,
+                        const TraversalConfig& config, SumStats* stats) {
+    if (sources.weights.size() != sources.positions.size())
+        throw std::invalid_argument("weight count does not match the tree's particle count");
+    const csfs_b200_kernel k = to_c(kernel);
+    const csfs_b200_config c{config.mac, config.degree, config.n0, config.shrink ? 1 : 0};
+    PotentialField f;
+    f.out_dim = kernel.out_dim();
+    f.values.resize(targets.size() * f.out_dim);
+    csfs_b200_stats st{};
+    const double* tx = targets.positions.empty() ? nullptr : &targets.positions[0].x;
+    const double* sx = sources.positions.empty() ? nullptr : &sources.positions[0].x;
+    check(csfs_b200_cstc(thread_ctx(), tx, targets.size(), sx, sources.weights.data(), sources.size(), &k, &c,
+                         f.values.data(), &st));
+    if (stats) {
+        *stats = SumStats{};
+        stats->t_tree_build = st.t_tree_build;
+        stats->t_upward = st.t_upward;
+        stats->t_traversal = st.t_traversal;
+        stats->t_total = st.t_total;
+        stats->pp = st.pp;
+        stats->pc = st.pc;
+        stats->source_tree.depth = st.src_depth;
+        stats->source_tree.cluster_count = st.src_clusters;
+        stats->source_tree.leaf_count = st.src_leaves;
+    }
+    return f;
+}
+
 PotentialField direct_sum(const ParticleSet& targets, const ParticleSet& sources, const Kernel& kernel,
                           int /*threads*/) {
     if (sources.weights.size() != sources.positions.size())
@@ -98,6 +127,28 @@ PotentialField direct_sum(const ParticleSet& targets, const ParticleSet& sources
     check(csfs_b200_direct(thread_ctx(), tx, targets.size(), sx, sources.weights.data(), sources.size(), &k,
                            f.values.data()));
     return f;
+}
+
+}  // namespace CSFS_B200_SHIM_NAMESPACE
+
+namespace CSFS_B200_SHIM_NAMESPACE {
+
+// summed_potential (summation.cpp:423-440): dispatch on config.method.
+csfs::PotentialField summed_potential(const csfs::ParticleSet& targets, const csfs::ParticleSet& sources,
+                                      const csfs::Kernel& kernel, const csfs::TraversalConfig& config,
+                                      csfs::SumStats* stats) {
+    switch (config.method) {
+        case csfs::Method::Direct: {
+            csfs::PotentialField f = direct_sum(targets, sources, kernel, config.threads);
+            if (stats) {
+                *stats = csfs::SumStats{};
+                stats->pp = targets.size() * sources.size();
+            }
+            return f;
+        }
+        case csfs::Method::Cstc: return cstc_sum(targets, sources, kernel, config, stats);
+        default: return csfmm_sum(targets, sources, kernel, config, stats);
+    }
 }
 
 }  // namespace CSFS_B200_SHIM_NAMESPACE

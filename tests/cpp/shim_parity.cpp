@@ -13,6 +13,8 @@ namespace csfs_gpu {
 csfs::PotentialField csfmm_sum(const csfs::ParticleSet&, const csfs::ParticleSet&, const csfs::Kernel&,
                                const csfs::TraversalConfig&, csfs::SumStats*);
 csfs::PotentialField direct_sum(const csfs::ParticleSet&, const csfs::ParticleSet&, const csfs::Kernel&, int);
+csfs::PotentialField summed_potential(const csfs::ParticleSet&, const csfs::ParticleSet&, const csfs::Kernel&,
+                                      const csfs::TraversalConfig&, csfs::SumStats*);
 }  // namespace csfs_gpu
 
 using namespace csfs;
@@ -65,6 +67,20 @@ int main() {
                                 csfs::direct_sum(p, p, Kernel::parse("sal"), 0));
         std::printf("direct_sal %.3e\n", e);
         if (!(e < 1e-12)) ++bad;
+    }
+    {  // summed_potential dispatch: the treecode
+        const SphericalGrid g = build_grid(GridKind::Icosahedral, 4);
+        ParticleSet p;
+        p.positions = g.centers;
+        p.weights.resize(g.size());
+        for (size_t i = 0; i < g.size(); ++i) p.weights[i] = real_sph_harm(4, 3, g.centers[i]) * g.areas[i];
+        TraversalConfig cfg;
+        cfg.method = Method::Cstc;
+        SumStats sg, sr;
+        const double e = rel_l2(csfs_gpu::summed_potential(p, p, Kernel::parse("sal"), cfg, &sg),
+                                csfs::summed_potential(p, p, Kernel::parse("sal"), cfg, &sr));
+        std::printf("cstc_sal %.3e %zu %zu | %zu %zu\n", e, sg.pp, sg.pc, sr.pp, sr.pc);
+        if (!(e < 1e-10) || sg.pp != sr.pp || sg.pc != sr.pc) ++bad;
     }
     {  // the reference's exception contract
         ParticleSet empty, one;
