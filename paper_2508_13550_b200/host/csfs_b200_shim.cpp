@@ -139,15 +139,15 @@ csfs::PotentialField summed_potential(const csfs::ParticleSet& targets, const cs
                                       csfs::SumStats* stats) {
     switch (config.method) {
         case csfs::Method::Direct: {
-            csfs::PotentialField f = direct_sum(targets, sources, kernel, config.threads);
+            csfs::PotentialField f = CSFS_B200_SHIM_NAMESPACE::direct_sum(targets, sources, kernel, config.threads);
             if (stats) {
                 *stats = csfs::SumStats{};
                 stats->pp = targets.size() * sources.size();
             }
             return f;
         }
-        case csfs::Method::Cstc: return cstc_sum(targets, sources, kernel, config, stats);
-        default: return csfmm_sum(targets, sources, kernel, config, stats);
+        case csfs::Method::Cstc: return CSFS_B200_SHIM_NAMESPACE::cstc_sum(targets, sources, kernel, config, stats);
+        default: return CSFS_B200_SHIM_NAMESPACE::csfmm_sum(targets, sources, kernel, config, stats);
     }
 }
 
