@@ -8,8 +8,10 @@
 //   level d : for every splitting node, quadrant keys, one global 4-counter scan, a
 //             single-CTA child allocator (children in parent order, empties pruned),
 //             and a scatter that keeps each node's range contiguous (K3)
-//   per level: shrunk bounds, centre and radius by warp-aggregated integer atomics on
-//             order-preserving encodings (exact, so deterministic)   (K4)
+//   per level: shrunk bounds and centre by warp-accumulated integer atomics on
+//             order-preserving encodings (exact, so deterministic)   (K4); only xi, eta,
+//             perm and node move between levels
+//   at the end: positions/weights gathered once through perm, every radius in one pass
 // Internal cluster ids are level-major (BFS); reference_ids() maps them onto the
 // reference's LIFO numbering for export (K5).  Particle data stays SoA in HBM.
 #include <algorithm>
@@ -212,36 +214,61 @@ __global__ void k_geom(int first, const int* nnew_dev, int cnt_host, ClusterPtrs
     if (sp) atomicAdd(nsplit, 1);
 }
 
-// Radius = max chordal distance from the centre to the cluster's particles (:67-69);
-// non-negative doubles order like their bit patterns.
-__global__ void k_radius(long long n, int first, const int* nnew_dev, int cnt_host,
-                         const int* __restrict__ node, const double* __restrict__ px,
-                         const double* __restrict__ py, const double* __restrict__ pz,
-                         const double* __restrict__ cx, const double* __restrict__ cy,
-                         const double* __restrict__ cz, double* rad) {
-    const int cnt = nnew_dev ? *nnew_dev : cnt_host;
+// Radii of every cluster once the tree is final (:67-69): positions are gathered into tree
+// order once, and each particle visits its ancestors level by level (deepest first);
+// kSegItems particles per thread keep their positions and current ancestor in registers.
+__global__ void k_radius_all(long long n, int max_depth, const int* __restrict__ node,
+                             const int* __restrict__ depth, const int* __restrict__ parent,
+                             const double* __restrict__ px, const double* __restrict__ py,
+                             const double* __restrict__ pz, const double* __restrict__ cx,
+                             const double* __restrict__ cy, const double* __restrict__ cz, double* rad) {
     const long long base = (long long)blockIdx.x * blockDim.x * kSegItems + threadIdx.x;
     constexpr int op[1] = {1};
     unsigned long long* radu = reinterpret_cast<unsigned long long*>(rad);
-    SegAcc<1> s;
+    double x[kSegItems], y[kSegItems], z[kSegItems];
+    int a[kSegItems];
+#pragma unroll
     for (int j = 0; j < kSegItems; ++j) {
         const long long i = base + (long long)j * blockDim.x;
-        int nd = -1;
-        unsigned long long val[1] = {0};
+        a[j] = -1;
+        x[j] = y[j] = z[j] = 0.0;
         if (i < n) {
-            nd = node[i];
-            if (nd >= first && nd < first + cnt) {
-                const double dx = __dsub_rn(cx[nd], px[i]);
-                const double dy = __dsub_rn(cy[nd], py[i]);
-                const double dz = __dsub_rn(cz[nd], pz[i]);
-                val[0] = __double_as_longlong(__dsqrt_rn(dot_ref(dx, dy, dz, dx, dy, dz)));
-            } else {
-                nd = -1;
-            }
+            a[j] = node[i];
+            x[j] = px[i];
+            y[j] = py[i];
+            z[j] = pz[i];
         }
-        seg_step<1>(s, nd, val, radu, op);
     }
-    seg_flush<1>(s, radu, op);
+    for (int L = max_depth; L >= 0; --L) {
+        SegAcc<1> s;
+#pragma unroll
+        for (int j = 0; j < kSegItems; ++j) {
+            int nd = -1;
+            unsigned long long val[1] = {0};
+            if (a[j] >= 0) {
+                while (depth[a[j]] > L) a[j] = parent[a[j]];
+                if (depth[a[j]] == L) {
+                    nd = a[j];
+                    const double dx = __dsub_rn(cx[nd], x[j]);
+                    const double dy = __dsub_rn(cy[nd], y[j]);
+                    const double dz = __dsub_rn(cz[nd], z[j]);
+                    val[0] = __double_as_longlong(__dsqrt_rn(dot_ref(dx, dy, dz, dx, dy, dz)));
+                }
+            }
+            seg_step<1>(s, nd, val, radu, op);
+        }
+        seg_flush<1>(s, radu, op);
+    }
+}
+
+__global__ void k_gather_xyz(long long n, const int* __restrict__ perm, const double* __restrict__ xyz,
+                             double* px, double* py, double* pz) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long q = perm[i];
+    px[i] = xyz[3 * q];
+    py[i] = xyz[3 * q + 1];
+    pz[i] = xyz[3 * q + 2];
 }
 
 // --- splitting (cluster_tree.cpp:87-141) ------------------------------------------------
@@ -335,9 +362,11 @@ __global__ void k_scatter(long long n, int first, int cnt, ClusterPtrs c, PartAr
         pos = koff[4 * f + q] + (rank[i] - segP[4 * f + q]);
         newnode = kid[4 * f + q];
     }
-    a.px2[pos] = a.px[i];
-    a.py2[pos] = a.py[i];
-    a.pz2[pos] = a.pz[i];
+    if (a.px) {
+        a.px2[pos] = a.px[i];
+        a.py2[pos] = a.py[i];
+        a.pz2[pos] = a.pz[i];
+    }
     a.xi2[pos] = x;
     a.eta2[pos] = e;
     a.perm2[pos] = a.perm[i];
@@ -397,9 +426,7 @@ void finish_level(DeviceTree& t, Scratch& sc, int first, const int* nnew_dev, in
     CSFS_CK(cudaMemsetAsync(sc.counters.p + 1, 0, sizeof(int), s));
     k_geom<<<gb, kThreads, 0, s>>>(first, nnew_dev, cnt_bound, c, t.shrink, t.n0, sc.counters.p + 1);
     CSFS_LAUNCH_CHECK();
-    k_radius<<<gs, kThreads, 0, s>>>(t.n, first, nnew_dev, cnt_bound, t.node, t.px, t.py, t.pz,
-                                      t.cx, t.cy, t.cz, t.rad);
-    CSFS_LAUNCH_CHECK();
+// radii: once for all levels after the build (k_radius_all)
 }
 
 template <class T>
@@ -512,9 +539,6 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
             int base = 0;
             for (int j = 0; j < k; ++j) base += grand[j];
             const long long p = base + pre[k];
-            px[p] = xyz[3 * i];
-            py[p] = xyz[3 * i + 1];
-            pz[p] = xyz[3 * i + 2];
             xi[p] = fxi[i];
             eta[p] = feta[i];
             perm[p] = int(i);
@@ -576,13 +600,11 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
                                                sc.koff, sc.counters.p);
         CSFS_LAUNCH_CHECK();
         // weights are not carried through the levels: gathered once via perm at the end
-        PartArrays a{t.px, t.py, t.pz, t.xi, t.eta, nullptr, t.perm, t.node, t.px2, t.py2, t.pz2, t.xi2,
-                     t.eta2, nullptr, t.perm2, t.node2};
+        // positions and weights are not carried through the levels: gathered once via perm
+        PartArrays a{nullptr, nullptr, nullptr, t.xi, t.eta, nullptr, t.perm, t.node, nullptr, nullptr, nullptr,
+                     t.xi2, t.eta2, nullptr, t.perm2, t.node2};
         k_scatter<<<gp, kThreads, 0, s>>>(n, first, cnt, c, a, t.rank, sc.segP, sc.kid, sc.koff);
         CSFS_LAUNCH_CHECK();
-        swap_buf(t.px, t.px2);
-        swap_buf(t.py, t.py2);
-        swap_buf(t.pz, t.pz2);
         swap_buf(t.xi, t.xi2);
         swap_buf(t.eta, t.eta2);
         swap_buf(t.perm, t.perm2);
@@ -597,6 +619,13 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
         t.level_first.push_back(next_id);
         t.level_count.push_back(nnew);
     }
+
+    // ---- positions in tree order, then every cluster's radius ------------------------------
+    k_gather_xyz<<<gp, kThreads, 0, s>>>(n, t.perm, xyz, t.px, t.py, t.pz);
+    CSFS_LAUNCH_CHECK();
+    k_radius_all<<<ceil_div(n, kThreads * kSegItems), kThreads, 0, s>>>(n, t.depth_max(), t.node, t.depth, t.parent,
+                                                                       t.px, t.py, t.pz, t.cx, t.cy, t.cz, t.rad);
+    CSFS_LAUNCH_CHECK();
 
     // ---- weights in tree order (permute_weights, summation.cpp:98-104) ---------------------
     if (t.has_w) {
