@@ -279,64 +279,44 @@ __device__ __forceinline__ int quadrant_of(const ClusterPtrs& c, int nd, double 
     return (x >= mx ? 1 : 0) + (e >= my ? 2 : 0);
 }
 
-// Single CTA: children of every splitting frontier node, allocated in frontier order and
-// quadrant order with empty quadrants pruned (:124-140).
-__global__ void __launch_bounds__(kScanThreads)
-    k_children(int first, int cnt, int next_id, ClusterPtrs c, const int* segP, const int* segE,
-               int* kid, int* koff, int* nnew) {
-    int carry = 0;
-    for (int f0 = 0; f0 < cnt; f0 += kScanThreads) {
-        const int f = f0 + threadIdx.x;
-        const int id = first + f;
-        const bool sp = f < cnt && c.split[id];
-        int cntk[4] = {0, 0, 0, 0};
-        int m[1] = {0};
-        if (sp) {
-            for (int k = 0; k < 4; ++k) {
-                cntk[k] = segE[4 * f + k] - segP[4 * f + k];
-                m[0] += cntk[k] > 0;
-            }
+// Children of splitting frontier node `id` (frontier index f), ids from `cid`, in quadrant
+// order with empty quadrants pruned (:124-140); records each quadrant's destination offset
+// and child id for the scatter.
+__device__ __forceinline__ void emit_children(const ClusterPtrs& c, int id, int f, int cid, const int* segP,
+                                              const int* segE, int* kid, int* koff) {
+    int acc = c.begin[id];
+    const double x0 = c.xi0[id], x1 = c.xi1[id], e0 = c.eta0[id], e1 = c.eta1[id];
+    const double mx = __dmul_rn(0.5, __dadd_rn(x0, x1));
+    const double my = __dmul_rn(0.5, __dadd_rn(e0, e1));
+    const double rx0[4] = {x0, mx, x0, mx}, rx1[4] = {mx, x1, mx, x1};
+    const double ry0[4] = {e0, e0, my, my}, ry1[4] = {my, my, e1, e1};
+    int ch[4] = {-1, -1, -1, -1};
+    int nch = 0;
+    const int fc = c.face[id], dp = c.depth[id] + 1;
+    for (int k = 0; k < 4; ++k) {
+        const int cntk = segE[4 * f + k] - segP[4 * f + k];
+        koff[4 * f + k] = acc;
+        kid[4 * f + k] = -1;
+        if (cntk > 0) {
+            c.face[cid] = fc;
+            c.depth[cid] = dp;
+            c.begin[cid] = acc;
+            c.end[cid] = acc + cntk;
+            c.parent[cid] = id;
+            c.nchild[cid] = 0;
+            c.child[cid] = make_int4(-1, -1, -1, -1);
+            c.xi0[cid] = rx0[k];
+            c.xi1[cid] = rx1[k];
+            c.eta0[cid] = ry0[k];
+            c.eta1[cid] = ry1[k];
+            kid[4 * f + k] = cid;
+            ch[nch++] = cid;
+            ++cid;
         }
-        int tot[1];
-        block_exclusive_scan<1>(m, tot);
-        if (sp) {
-            int cid = next_id + carry + m[0];
-            int acc = c.begin[id];
-            const double x0 = c.xi0[id], x1 = c.xi1[id], e0 = c.eta0[id], e1 = c.eta1[id];
-            const double mx = __dmul_rn(0.5, __dadd_rn(x0, x1));
-            const double my = __dmul_rn(0.5, __dadd_rn(e0, e1));
-            const double rx0[4] = {x0, mx, x0, mx}, rx1[4] = {mx, x1, mx, x1};
-            const double ry0[4] = {e0, e0, my, my}, ry1[4] = {my, my, e1, e1};
-            int ch[4] = {-1, -1, -1, -1};
-            int nch = 0;
-            const int fc = c.face[id], dp = c.depth[id] + 1;
-            for (int k = 0; k < 4; ++k) {
-                koff[4 * f + k] = acc;
-                kid[4 * f + k] = -1;
-                if (cntk[k] > 0) {
-                    c.face[cid] = fc;
-                    c.depth[cid] = dp;
-                    c.begin[cid] = acc;
-                    c.end[cid] = acc + cntk[k];
-                    c.parent[cid] = id;
-                    c.nchild[cid] = 0;
-                    c.child[cid] = make_int4(-1, -1, -1, -1);
-                    c.xi0[cid] = rx0[k];
-                    c.xi1[cid] = rx1[k];
-                    c.eta0[cid] = ry0[k];
-                    c.eta1[cid] = ry1[k];
-                    kid[4 * f + k] = cid;
-                    ch[nch++] = cid;
-                    ++cid;
-                }
-                acc += cntk[k];
-            }
-            c.child[id] = make_int4(ch[0], ch[1], ch[2], ch[3]);
-            c.nchild[id] = nch;
-        }
-        carry += tot[0];
+        acc += cntk;
     }
-    if (threadIdx.x == 0) *nnew = carry;
+    c.child[id] = make_int4(ch[0], ch[1], ch[2], ch[3]);
+    c.nchild[id] = nch;
 }
 
 struct PartArrays {
@@ -596,9 +576,23 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
             };
             run_scan<4>(n, f, e, sc.tiles, sc.grand, s);
         }
-        k_children<<<1, kScanThreads, 0, s>>>(first, cnt, next_id, c, sc.segP, sc.segE, sc.kid,
-                                               sc.koff, sc.counters.p);
-        CSFS_LAUNCH_CHECK();
+        {  // child allocation: a scan over the frontier of non-empty quadrant counts
+            const int* segP = sc.segP;
+            const int* segE = sc.segE;
+            int* kid = sc.kid;
+            int* koff = sc.koff;
+            auto f = [=] __device__(long long fi, int* cc) {
+                if (!c.split[first + fi]) return;
+                int m = 0;
+                for (int k = 0; k < 4; ++k) m += (segE[4 * fi + k] - segP[4 * fi + k]) > 0;
+                cc[0] = m;
+            };
+            auto e = [=] __device__(long long fi, const int* cc, const int* pre) {
+                if (c.split[first + fi]) emit_children(c, first + int(fi), int(fi), next_id + pre[0], segP, segE, kid, koff);
+            };
+            run_scan<1>(cnt, f, e, sc.tiles, sc.grand, s);
+            CSFS_CK(cudaMemcpyAsync(sc.counters.p, sc.grand.p, sizeof(int), cudaMemcpyDeviceToDevice, s));
+        }
         // weights are not carried through the levels: gathered once via perm at the end
         // positions and weights are not carried through the levels: gathered once via perm
         PartArrays a{nullptr, nullptr, nullptr, t.xi, t.eta, nullptr, t.perm, t.node, nullptr, nullptr, nullptr,
