@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2508_13550_b200 import Kernel, TraversalConfig, configs
+from paper_2508_13550_b200 import Kernel, ParticleSet, TraversalConfig, configs
 from paper_2508_13550_b200.distributed import plan_partition
 
 pytestmark = pytest.mark.gpu
@@ -55,3 +55,17 @@ def test_partition_bitwise(engine, name, level, kname):
         rngs = [p.target_range for p in plans if p.target_range[1] > p.target_range[0]]
         assert rngs[0][0] == 0 and rngs[-1][1] == wl.n
         assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
+
+
+@pytest.mark.parametrize("name,level", [("c5", 7), ("c3", 7), ("c4", 7)])
+def test_run_to_run_bitwise(engine, name, level):
+    """Every output slot has one owner and a fixed summation order (no atomics on
+    floating-point data), so repeated runs are bitwise identical — the reference's
+    thread-count independence claim (summation.hpp:19-21) on the GPU, and a race check."""
+    wl = configs.make(name, level=level)
+    p = ParticleSet(wl.xyz, wl.weights)
+    cfg = TraversalConfig(mac=wl.mac, degree=wl.degree, n0=wl.n0)
+    k = Kernel.parse(wl.kernel)
+    a = engine.csfmm_sum(p, p, k, cfg).values
+    b = engine.csfmm_sum(p, p, k, cfg).values
+    np.testing.assert_array_equal(a, b)
