@@ -67,7 +67,7 @@ __device__ __forceinline__ LogTable stage_log_table(double2* s_rl, double* s_lo,
 #define CSFS_MINB 2
 #endif
 #ifndef CSFS_UNROLL
-#define CSFS_UNROLL 2
+#define CSFS_UNROLL 8
 #endif
 constexpr int kIB = CSFS_IB;    // threads per CTA
 constexpr int kTPT = CSFS_TPT;  // targets per thread
