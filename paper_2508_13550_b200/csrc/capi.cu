@@ -278,10 +278,10 @@ int csfs_b200_create(csfs_b200_ctx** out, int device) {
         CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
         const char* nosym = std::getenv("CSFS_B200_NO_SYMMETRIC");
         c->use_mutual = !(nosym && nosym[0] == '1');
-        std::vector<double2> tab(2 * kLogTab);
+        std::vector<double2> tab(kLogTabWords);
         make_log_table(tab.data());
-        c->log_tab.grow(2 * kLogTab);
-        CSFS_CK(cudaMemcpy(c->log_tab.p, tab.data(), 2 * kLogTab * sizeof(double2), cudaMemcpyHostToDevice));
+        c->log_tab.grow(kLogTabWords);
+        CSFS_CK(cudaMemcpy(c->log_tab.p, tab.data(), kLogTabWords * sizeof(double2), cudaMemcpyHostToDevice));
     });
     if (rc != CSFS_B200_OK) {
         // keep the context alive only to report the error? The caller gets NULL.

@@ -23,8 +23,15 @@ constexpr double kCoincidenceTol = 1e-14;  // kernels.hpp:28
 constexpr double kNodeTol = 1e-14;         // interpolation.cpp:8
 constexpr int kMaxDepth = 60;              // cluster_tree.cpp:11
 constexpr double kMinExtent = 1e-13;       // cluster_tree.cpp:12
-constexpr int kLogTabBits = 8;             // fastmath.cuh log table: 256 entries
+#ifndef CSFS_LOG_BITS
+#define CSFS_LOG_BITS 9
+#endif
+#ifndef CSFS_LOG_PACK
+#define CSFS_LOG_PACK 1
+#endif
+constexpr int kLogTabBits = CSFS_LOG_BITS;  // fastmath.cuh log table: 2^bits mantissa intervals
 constexpr int kLogTab = 1 << kLogTabBits;
+constexpr int kLogTabWords = CSFS_LOG_PACK ? kLogTab : 2 * kLogTab;  // double2 words (global)
 
 // Error classes that map onto the C-ABI return codes (include/csfs_b200.h).
 struct InvalidArgument : std::runtime_error {
@@ -68,6 +75,20 @@ struct Cheb {
 __device__ __forceinline__ double dot_ref(double ax, double ay, double az, double bx, double by,
                                           double bz) {
     return __dadd_rn(__dadd_rn(__dmul_rn(ax, bx), __dmul_rn(ay, by)), __dmul_rn(az, bz));
+}
+
+// !(omc < kCoincidenceTol) (kernels.hpp:28) on the integer pipe: for IEEE doubles the
+// signed 64-bit order of the bit patterns equals the numeric order on non-negative values,
+// and every negative value (sign bit set, incl. -0.0) compares below the positive
+// threshold, as it does numerically.  Saves a DSETP per pair on the FP64 pipe.
+__device__ __forceinline__ bool not_coincident(double omc) {
+    return __double_as_longlong(omc) >= __double_as_longlong(kCoincidenceTol);
+}
+
+// `ok ? omc : (a value in [1, 1 + 2^-20))` with a single 32-bit select: the skipped pair
+// only needs a safe finite argument for the log / rsqrt / rcp that follow.
+__device__ __forceinline__ double safe_omc(bool ok, double omc) {
+    return __hiloint2double(ok ? __double2hiint(omc) : 0x3ff00000, __double2loint(omc));
 }
 
 // bary_basis_1d (interpolation.cpp:26-43), same node test, same summation order.

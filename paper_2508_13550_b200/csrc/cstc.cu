@@ -27,13 +27,8 @@ __global__ void __launch_bounds__(kCstcThreads)
            const double* __restrict__ sw, const double* __restrict__ qw, double mac, int n0, Op op,
            const double2* __restrict__ log_tab, double* __restrict__ out, unsigned long long* counts) {
     constexpr int D = Op::dim;
-    __shared__ double2 tab_rl[kLogTab];
-    __shared__ double tab_lo[kLogTab];
-    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) {
-        tab_rl[i] = log_tab[i];
-        tab_lo[i] = log_tab[kLogTab + i].x;
-    }
-    const LogTable tab{tab_rl, tab_lo};
+    __shared__ LogTableSmem tab_sm;
+    const LogTable tab = stage_log_table(tab_sm, log_tab);
     __syncthreads();
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long npp_ = 0, npc = 0;
@@ -86,21 +81,6 @@ __global__ void __launch_bounds__(kCstcThreads)
     }
 }
 
-template <class F>
-void with_op_cstc(const KernelSpec& k, F&& f) {
-    switch (k.kind) {
-        case 0: f(OpLaplace{}); break;
-        case 1: f(OpBiharmonic{}); break;
-        case 2: f(OpBiotSavart{}); break;
-        default: {
-            OpSal op;
-            op.pref = 3.0 * k.rho_ratio * kInv4Pi;
-            op.c1 = 1.0 - k.b0;
-            op.c2 = k.a1 - k.b1;
-            f(op);
-        }
-    }
-}
 
 }  // namespace
 
@@ -110,7 +90,7 @@ void cstc_eval(const KernelSpec& k, const double* txyz, long long nt, const int*
     if (nt == 0) return;
     CSFS_CK(cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), s));
     const TreeView S = src.view();
-    with_op_cstc(k, [&](auto op) {
+    with_op(k, [&](auto op) {
         k_cstc<<<ceil_div(nt, kCstcThreads), kCstcThreads, 0, s>>>(txyz, nt, order, S, src.w, src.qw, mac, n0, op,
                                                                     log_tab, out, counts);
         CSFS_LAUNCH_CHECK();

@@ -17,45 +17,55 @@
 // This is FP64-pipe bound: the inner loop is the kernel functor.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "engine.hpp"
 #include "kernels_dev.cuh"
 
 namespace csfs_b200 {
 
-// tab[i] = {r_i, L_hi_i}, tab[kLogTab + i] = {L_lo_i, 0}: r_i = 1/(1 + (i + 1/2)/256),
-// except r_0 = 1 (m in [1, 1+2^-8)) and r_255 = 1/2 (m in [2-2^-8, 2)), where m r - 1 is
-// exact; -ln r_i = L_hi + L_lo with L_hi on the 2^-42 grid (exact sums with e*ln2_hi),
-// from long-double logl (64-bit mantissa) so L_lo is good to ~1e-19.  The r = 1/2 entry
-// uses exactly the split of ln 2 the device code uses, so e*ln2 + L cancels exactly.
+// fastmath.cuh table: r_i ~ 1/(1 + (i + 1/2)/kLogTab) rounded to 21 significant bits,
+// except r_0 = 1 (m in [1, 1 + 2^-9)) and r_last = 1/2 (m in [2 - 2^-9, 2)), where m r - 1
+// is exact; -ln r_i (of the rounded r_i, from long-double logl: 64-bit mantissa) =
+// L_hi + L_lo with L_hi on the 2^-42 grid (exact sums with e*ln2_hi) and L_lo rounded to
+// 21 bits (|err| <= 2^-64).  The r = 1/2 entry holds exactly the device's split of ln 2, so
+// e*ln2 + L cancels exactly at e = -1.
+static double round_hi_word(double v) {  // v rounded to the 21 significant bits of its high word
+    if (v == 0.0) return 0.0;
+    int ex = 0;
+    const double f = std::frexp(v, &ex);  // v = f 2^ex, |f| in [1/2, 1)
+    return std::ldexp(std::nearbyint(std::ldexp(f, 21)), ex - 21);
+}
+
 void make_log_table(double2* tab) {
     for (int i = 0; i < kLogTab; ++i) {
-        double r = 1.0 / (1.0 + (i + 0.5) / kLogTab);
+        double r = round_hi_word(1.0 / (1.0 + (i + 0.5) / kLogTab));
         if (i == 0) r = 1.0;
         if (i == kLogTab - 1) r = 0.5;
         const long double L = -logl((long double)r);
         double hi = double(nearbyintl(L * 0x1p42L) / 0x1p42L);
-        double lo = double(L - (long double)hi);
+        double lo = round_hi_word(double(L - (long double)hi));
         if (i == 0) hi = lo = 0.0;
         if (i == kLogTab - 1) {
-            hi = 0x1.62e42fefa3800p-1;  // fastmath.cuh kLn2Hi / kLn2Lo
-            lo = 0x1.ef35793c76730p-45;
+            hi = kLn2Hi;
+            lo = kLn2Lo;
         }
-        tab[i] = make_double2(r, hi);
+#if CSFS_LOG_PACK
+        unsigned long long rb, lb;
+        std::memcpy(&rb, &r, 8);
+        std::memcpy(&lb, &lo, 8);
+        const unsigned long long w = (rb & 0xffffffff00000000ull) | (lb >> 32);
+        double wd;
+        std::memcpy(&wd, &w, 8);
+        tab[i] = make_double2(hi, wd);
+#else
+        tab[i] = make_double2(hi, r);
         tab[kLogTab + i] = make_double2(lo, 0.0);
+#endif
     }
 }
 
 namespace {
-
-// Copies the global log table into shared memory; caller syncs before use.
-__device__ __forceinline__ LogTable stage_log_table(double2* s_rl, double* s_lo, const double2* g) {
-    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) {
-        s_rl[i] = g[i];
-        s_lo[i] = g[kLogTab + i].x;
-    }
-    return LogTable{s_rl, s_lo};
-}
 
 #ifndef CSFS_IB
 #define CSFS_IB 256
@@ -91,7 +101,7 @@ struct InteractParams {
     double* out_q;  // proxy potentials (ncl_t x npp x dim)
     const int* anchor;  // per item owner key (nullptr: every item is ours)
     long long own_b, own_e;
-    const double2* log_tab;  // 2 x kLogTab entries (fastmath.cuh)
+    const double2* log_tab;  // kLogTabWords entries (fastmath.cuh)
 };
 
 template <class Op>
@@ -99,11 +109,10 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
     constexpr int D = Op::dim;
     __shared__ double2 sxy[kICH], szw[kICH];
     __shared__ double red[kIB * kTPT * D];
-    __shared__ double2 tab_rl[kLogTab];
-    __shared__ double tab_lo[kLogTab];
+    __shared__ LogTableSmem tab_sm;
     __shared__ int item_sh;
     const int tid = threadIdx.x;
-    const LogTable tab = stage_log_table(tab_rl, tab_lo, P.log_tab);  // synced by the loop's first barrier
+    const LogTable tab = stage_log_table(tab_sm, P.log_tab);  // synced by the loop's first barrier
     for (;;) {
         if (tid == 0) item_sh = atomicAdd(P.counter, 1);
         __syncthreads();
@@ -239,6 +248,7 @@ struct MutualParams {
     const long long* poff;  // partial offset of A's block (B's follows at + |A|)
     const int* anchor;      // A's begin, or -1: every rank
     int n_pairs;
+    int* counter;  // work queue (persistent CTAs)
     const double *px, *py, *pz, *pw;  // particles (tree order) + weights
     double* partial;
     const double2* log_tab;
@@ -251,118 +261,124 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
     __shared__ double2 sxy[kICH], szw[kICH];
     __shared__ double colbuf[kIB / 32][kICH];
     __shared__ double red[kIB * kMTPT];
-    __shared__ double2 tab_rl[kLogTab];
-    __shared__ double tab_lo[kLogTab];
-    const int p = blockIdx.x;
+    __shared__ LogTableSmem tab_sm;
+    __shared__ int pair_sh;
     const int tid = threadIdx.x, lane = tid & 31;
-    const LogTable tab = stage_log_table(tab_rl, tab_lo, P.log_tab);
-    const int4 q = P.pair[p];
-    if (P.anchor) {
-        const long long a = P.anchor[p];
-        if (a >= 0 && (a < P.own_b || a >= P.own_e)) return;  // CTA-uniform
-    }
-    for (int j = tid; j < q.w; j += kIB) {
-        sxy[j] = make_double2(P.px[q.z + j], P.py[q.z + j]);
-        szw[j] = make_double2(P.pz[q.z + j], P.pw[q.z + j]);
-    }
-    const int tlen = q.y, nb = q.w;
-    const int per = (tlen + kMTPT - 1) / kMTPT;
-    const int gs = min(kIB, (per + 31) & ~31);
-    const int G = kIB / gs;
-    const int g = tid / gs, r = tid - g * gs, wig = r >> 5;
-    const bool grp = g < G;
-    double tx[kMTPT], ty[kMTPT], tz[kMTPT], tw[kMTPT], acc[kMTPT];
-    bool act[kMTPT];
-#pragma unroll
-    for (int k = 0; k < kMTPT; ++k) {
-        const int t = r + k * gs;
-        act[k] = grp && t < tlen;
-        tx[k] = 0.0;
-        ty[k] = 0.0;
-        tz[k] = 1.0;
-        tw[k] = 0.0;
-        if (act[k]) {
-            tx[k] = P.px[q.x + t];
-            ty[k] = P.py[q.x + t];
-            tz[k] = P.pz[q.x + t];
-            tw[k] = P.pw[q.x + t];
+    const LogTable tab = stage_log_table(tab_sm, P.log_tab);  // synced by the loop's first barrier
+    for (;;) {
+        if (tid == 0) pair_sh = atomicAdd(P.counter, 1);
+        __syncthreads();  // also: the previous pair's shared-memory reads are done
+        const int p = pair_sh;
+        __syncthreads();
+        if (p >= P.n_pairs) break;
+        if (P.anchor) {
+            const long long a = P.anchor[p];
+            if (a >= 0 && (a < P.own_b || a >= P.own_e)) continue;  // CTA-uniform
         }
-        acc[k] = 0.0;
-    }
-    __syncthreads();
-    if (grp) {
-        // 8 sources (j + m*G, m < 8) per step; their per-thread column partials are reduced
-        // over the warp by a transposed butterfly: 4+2+1+1+1 shuffles for 8 sources
-        constexpr int kB = 8;
-        const int full_end = nb - (kB - 1) * G;  // j < full_end: all 8 sources exist
-        auto sources = [&](int j, double (&c)[kB], bool guard) {
+        const int4 q = P.pair[p];
+        for (int j = tid; j < q.w; j += kIB) {
+            sxy[j] = make_double2(P.px[q.z + j], P.py[q.z + j]);
+            szw[j] = make_double2(P.pz[q.z + j], P.pw[q.z + j]);
+        }
+        const int tlen = q.y, nb = q.w;
+        const int per = (tlen + kMTPT - 1) / kMTPT;
+        const int gs = min(kIB, (per + 31) & ~31);
+        const int G = kIB / gs;
+        const int g = tid / gs, r = tid - g * gs, wig = r >> 5;
+        const bool grp = g < G;
+        double tx[kMTPT], ty[kMTPT], tz[kMTPT], tw[kMTPT], acc[kMTPT];
+        bool act[kMTPT];
 #pragma unroll
-            for (int m = 0; m < kB; ++m) {
-                c[m] = 0.0;
-                const int jm = j + m * G;
-                if (!guard || jm < nb) {  // group-uniform
-                    const double2 a = sxy[jm], b = szw[jm];
+        for (int k = 0; k < kMTPT; ++k) {
+            const int t = r + k * gs;
+            act[k] = grp && t < tlen;
+            tx[k] = 0.0;
+            ty[k] = 0.0;
+            tz[k] = 1.0;
+            tw[k] = 0.0;
+            if (act[k]) {
+                tx[k] = P.px[q.x + t];
+                ty[k] = P.py[q.x + t];
+                tz[k] = P.pz[q.x + t];
+                tw[k] = P.pw[q.x + t];
+            }
+            acc[k] = 0.0;
+        }
+        __syncthreads();
+        if (grp) {
+            // 8 sources (j + m*G, m < 8) per step; their per-thread column partials are reduced
+            // over the warp by a transposed butterfly: 4+2+1+1+1 shuffles for 8 sources
+            constexpr int kB = 8;
+            const int full_end = nb - (kB - 1) * G;  // j < full_end: all 8 sources exist
+            auto sources = [&](int j, double (&c)[kB], bool guard) {
 #pragma unroll
-                    for (int k = 0; k < kMTPT; ++k) {
-                        double K[1];
-                        op.value(tx[k], ty[k], tz[k], a.x, a.y, b.x, K, tab);
-                        acc[k] = fma(b.y, K[0], acc[k]);
-                        c[m] = fma(tw[k], K[0], c[m]);
+                for (int m = 0; m < kB; ++m) {
+                    c[m] = 0.0;
+                    const int jm = j + m * G;
+                    if (!guard || jm < nb) {  // group-uniform
+                        const double2 a = sxy[jm], b = szw[jm];
+#pragma unroll
+                        for (int k = 0; k < kMTPT; ++k) {
+                            double K[1];
+                            op.value(tx[k], ty[k], tz[k], a.x, a.y, b.x, K, tab);
+                            acc[k] = fma(b.y, K[0], acc[k]);
+                            c[m] = fma(tw[k], K[0], c[m]);
+                        }
                     }
                 }
-            }
-        };
-        for (int j = g; j < nb; j += kB * G) {
-            double c[kB];
-            if (j < full_end) sources(j, c, false);
-            else sources(j, c, true);
-            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-            double v4[4], v2[2];
+            };
+            for (int j = g; j < nb; j += kB * G) {
+                double c[kB];
+                if (j < full_end) sources(j, c, false);
+                else sources(j, c, true);
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                double v4[4], v2[2];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {  // lanes < 16 keep sources 0..3, >= 16 keep 4..7
-                const double keep = b4 ? c[m + 4] : c[m];
-                const double send = b4 ? c[m] : c[m + 4];
-                v4[m] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-            }
+                for (int m = 0; m < 4; ++m) {  // lanes < 16 keep sources 0..3, >= 16 keep 4..7
+                    const double keep = b4 ? c[m + 4] : c[m];
+                    const double send = b4 ? c[m] : c[m + 4];
+                    v4[m] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                }
 #pragma unroll
-            for (int m = 0; m < 2; ++m) {
-                const double keep = b3 ? v4[m + 2] : v4[m];
-                const double send = b3 ? v4[m] : v4[m + 2];
-                v2[m] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                for (int m = 0; m < 2; ++m) {
+                    const double keep = b3 ? v4[m + 2] : v4[m];
+                    const double send = b3 ? v4[m] : v4[m + 2];
+                    v2[m] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+                double v = (b2 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? v2[0] : v2[1], 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                const int m = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+                const int jm = j + m * G;
+                if ((lane & 3) == 0 && jm < nb) colbuf[wig][jm] = v;
             }
-            double v = (b2 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? v2[0] : v2[1], 4);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            const int m = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
-            const int jm = j + m * G;
-            if ((lane & 3) == 0 && jm < nb) colbuf[wig][jm] = v;
         }
-    }
-    // rows: combine the G groups (fixed order), then write A's block
-    if (G > 1) {
-#pragma unroll
-        for (int k = 0; k < kMTPT; ++k)
-            if (act[k]) red[(g * gs + r) * kMTPT + k] = acc[k];
-    }
-    __syncthreads();
-    if (G > 1 && g == 0)
-        for (int h = 1; h < G; ++h)
+        // rows: combine the G groups (fixed order), then write A's block
+        if (G > 1) {
 #pragma unroll
             for (int k = 0; k < kMTPT; ++k)
-                if (act[k]) acc[k] += red[(h * gs + r) * kMTPT + k];
-    const long long base = P.poff[p];
-    if (g == 0) {
+                if (act[k]) red[(g * gs + r) * kMTPT + k] = acc[k];
+        }
+        __syncthreads();
+        if (G > 1 && g == 0)
+            for (int h = 1; h < G; ++h)
 #pragma unroll
-        for (int k = 0; k < kMTPT; ++k)
-            if (act[k]) P.partial[base + r + k * gs] = acc[k] * op.scale();
-    }
-    // columns: source j was handled by group j % G, whose warps wrote colbuf[0..W)[j]
-    const int W = gs >> 5;
-    const double f = op.scale() * Op::kSym;
-    for (int j = tid; j < nb; j += kIB) {
-        double v = 0.0;
-        for (int w = 0; w < W; ++w) v += colbuf[w][j];
-        P.partial[base + tlen + j] = v * f;
+                for (int k = 0; k < kMTPT; ++k)
+                    if (act[k]) acc[k] += red[(h * gs + r) * kMTPT + k];
+        const long long base = P.poff[p];
+        if (g == 0) {
+#pragma unroll
+            for (int k = 0; k < kMTPT; ++k)
+                if (act[k]) P.partial[base + r + k * gs] = acc[k] * op.scale();
+        }
+        // columns: source j was handled by group j % G, whose warps wrote colbuf[0..W)[j]
+        const int W = gs >> 5;
+        const double f = op.scale() * Op::kSym;
+        for (int j = tid; j < nb; j += kIB) {
+            double v = 0.0;
+            for (int w = 0; w < W; ++w) v += colbuf[w][j];
+            P.partial[base + tlen + j] = v * f;
+        }
     }
 }
 
@@ -405,9 +421,8 @@ __global__ void k_direct_items(int n_items, long long nt, int4* item, int nseg) 
 template <class Op>
 __global__ void k_eval_pairs(Op op, const double* x, const double* y, long long n, double* out,
                              const double2* log_tab) {
-    __shared__ double2 tab_rl[kLogTab];
-    __shared__ double tab_lo[kLogTab];
-    const LogTable tab = stage_log_table(tab_rl, tab_lo, log_tab);
+    __shared__ LogTableSmem tab_sm;
+    const LogTable tab = stage_log_table(tab_sm, log_tab);
     __syncthreads();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -417,9 +432,8 @@ __global__ void k_eval_pairs(Op op, const double* x, const double* y, long long 
 }
 
 __global__ void k_eval_math(int fn, const double* x, long long n, double* out, const double2* log_tab) {
-    __shared__ double2 tab_rl[kLogTab];
-    __shared__ double tab_lo[kLogTab];
-    const LogTable tab = stage_log_table(tab_rl, tab_lo, log_tab);
+    __shared__ LogTableSmem tab_sm;
+    const LogTable tab = stage_log_table(tab_sm, log_tab);
     __syncthreads();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -434,21 +448,6 @@ __global__ void k_eval_math(int fn, const double* x, long long n, double* out, c
     out[i] = r;
 }
 
-template <class F>
-void with_op(const KernelSpec& k, F&& f) {
-    switch (k.kind) {
-        case 0: f(OpLaplace{}); break;
-        case 1: f(OpBiharmonic{}); break;
-        case 2: f(OpBiotSavart{}); break;
-        default: {
-            OpSal op;
-            op.pref = 3.0 * k.rho_ratio * kInv4Pi;
-            op.c1 = 1.0 - k.b0;
-            op.c2 = k.a1 - k.b1;
-            f(op);
-        }
-    }
-}
 
 template <class Op>
 int grid_for(int n_items) {
@@ -471,7 +470,16 @@ template <class Op>
 void launch_mutual(const MutualParams& m, const Op& op, cudaStream_t s) {
     if constexpr (Op::dim == 1) {
         if (m.n_pairs == 0) return;
-        k_mutual<Op><<<m.n_pairs, kIB, 0, s>>>(m, op);
+        CSFS_CK(cudaMemsetAsync(m.counter, 0, sizeof(int), s));
+        int dev = 0, sms = 0, per = 0;
+        CSFS_CK(cudaGetDevice(&dev));
+        CSFS_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CSFS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mutual<Op>, kIB, 0));
+#ifndef CSFS_MUTUAL_PERSIST
+#define CSFS_MUTUAL_PERSIST 1
+#endif
+        const int grid = CSFS_MUTUAL_PERSIST ? std::max(1, std::min(m.n_pairs, sms * std::max(per, 1))) : m.n_pairs;
+        k_mutual<Op><<<grid, kIB, 0, s>>>(m, op);
         CSFS_LAUNCH_CHECK();
     }
 }
@@ -513,6 +521,7 @@ void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src,
         m.poff = items.mpoff;
         m.anchor = everything ? nullptr : items.manchor.p;
         m.n_pairs = items.n_mutual;
+        m.counter = work_counter + 1;
         m.px = src.px;
         m.py = src.py;
         m.pz = src.pz;

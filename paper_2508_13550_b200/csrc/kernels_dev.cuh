@@ -7,9 +7,10 @@
 //  * `x.y` and `1 - x.y` are evaluated unfused in the reference's order (dot_ref), so the
 //    near-neighbour cancellation is identical to the reference's build;
 //  * the coincidence guard `1 - x.y < 1e-14` is predicated (a safe argument is evaluated
-//    and the weight zeroed) instead of branched: no divergence, exact skip semantics;
+//    and the weight zeroed) instead of branched: no divergence, exact skip semantics; the
+//    compare itself runs on the integer pipe (not_coincident, common.cuh);
 //  * the prefactor (-1/4pi, 1/4pi, 3 rho/4pi) is applied once per target (`scale`);
-//  * log / rsqrt / rcp come from fastmath.cuh (13 / 5 / 3 FP64 instructions instead of
+//  * log / rsqrt / rcp come from fastmath.cuh (11 / 5 / 3 FP64 instructions instead of
 //    libdevice's ~28 / 8+8 / 8), each within a few ulp;
 //  * SAL: 1/gamma = rsqrt(2 omc), s = gamma/2 = omc * rsqrt(2 omc) (halving is exact),
 //    log(s (1 + s)) = log(fma(s, s, s)) — the reference's formula, without sqrt or divide.
@@ -31,16 +32,16 @@ struct OpLaplace {
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = !(omc < kCoincidenceTol);
-        const double v = fast_log(ok ? omc : 1.0, tab);
+        const bool ok = not_coincident(omc);
+        const double v = fast_log(safe_omc(ok, omc), tab);
         K[0] = ok ? v : 0.0;
     }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,
                                                const LogTable& tab) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = !(omc < kCoincidenceTol);
-        const double v = fast_log(ok ? omc : 1.0, tab);
+        const bool ok = not_coincident(omc);
+        const double v = fast_log(safe_omc(ok, omc), tab);
         acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
     }
 };
@@ -110,8 +111,8 @@ struct OpBiotSavart {
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable&) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = !(omc < kCoincidenceTol);
-        const double a = ok ? fast_rcp(ok ? omc : 1.0) : 0.0;
+        const bool ok = not_coincident(omc);
+        const double a = ok ? fast_rcp(safe_omc(ok, omc)) : 0.0;
         K[0] = a * __dsub_rn(__dmul_rn(ty, sz), __dmul_rn(tz, sy));
         K[1] = a * __dsub_rn(__dmul_rn(tz, sx), __dmul_rn(tx, sz));
         K[2] = a * __dsub_rn(__dmul_rn(tx, sy), __dmul_rn(ty, sx));
@@ -120,8 +121,8 @@ struct OpBiotSavart {
                                                double sz, double sw, double* acc,
                                                const LogTable&) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = !(omc < kCoincidenceTol);
-        const double a = (ok ? sw : 0.0) * fast_rcp(ok ? omc : 1.0);
+        const bool ok = not_coincident(omc);
+        const double a = (ok ? sw : 0.0) * fast_rcp(safe_omc(ok, omc));
         // cross(x, y) unfused, in the reference's order (geometry.hpp:20-22): for close
         // pairs the components cancel, and a contracted form would differ from it
         const double cx = __dsub_rn(__dmul_rn(ty, sz), __dmul_rn(tz, sy));
@@ -133,32 +134,65 @@ struct OpBiotSavart {
     }
 };
 
-struct OpSal {
+// SalOp (summation.cpp:63-76): pref (c1/gamma - c2 log(s (1 + s))), gamma = sqrt(2 omc),
+// s = gamma/2.  The constant c1 is folded into scale() (one FMA per pair instead of a
+// multiply and an FMA): K' = 1/gamma + k log(s (1 + s)), k = -c2/c1, scale = pref c1.  The
+// c1 == 0 case (pure log kernel) is the kLogOnly instantiation: K' = log(...), scale = -pref c2.
+template <bool kLogOnly>
+struct OpSalT {
     static constexpr int dim = 1;
     static constexpr double kSym = 1.0;
-    double pref, c1, c2;  // SalOp (summation.cpp:64-68)
-    __device__ __forceinline__ double scale() const { return pref; }
+    double scale_, k;
+    __host__ static OpSalT make(double pref, double c1, double c2) {
+        OpSalT op;
+        op.scale_ = kLogOnly ? -pref * c2 : pref * c1;
+        op.k = kLogOnly ? 0.0 : -c2 / c1;
+        return op;
+    }
+    __device__ __forceinline__ double scale() const { return scale_; }
+    // r = 1/gamma: MUFU seed of 2 omc (exponent + 1 on the integer pipe), then the cubic
+    // correction written on omc itself: e/2 = 1/2 - omc y^2 (no FP64 doubling).
+    __device__ __forceinline__ double kernel(double omc, const LogTable& tab) const {
+        const double y = rsqrt_seed(__hiloint2double(__double2hiint(omc) + 0x00100000, __double2loint(omc)));
+        const double h = omc * y;
+        const double eh = fma(-h, y, 0.5);
+        const double r = fma(y, eh * fma(eh, 1.5, 1.0), y);  // y (1 + e/2 + 3e^2/8)
+        const double s = omc * r;                              // gamma/2
+        const double L = fast_log(fma(s, s, s), tab);
+        return kLogOnly ? L : fma(k, L, r);
+    }
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
-        const double omc0 = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = !(omc0 < kCoincidenceTol);
-        const double omc = ok ? omc0 : 1.0;
-        const double r = fast_rsqrt(omc + omc);
-        const double s = omc * r;
-        const double v = fma(-c2, fast_log(fma(s, s, s), tab), c1 * r);
+        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = not_coincident(omc);
+        const double v = kernel(safe_omc(ok, omc), tab);
         K[0] = ok ? v : 0.0;
     }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,
                                                const LogTable& tab) const {
-        const double omc0 = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = !(omc0 < kCoincidenceTol);
-        const double omc = ok ? omc0 : 1.0;
-        const double r = fast_rsqrt(omc + omc);  // 1/gamma
-        const double s = omc * r;                 // gamma/2
-        const double v = fma(-c2, fast_log(fma(s, s, s), tab), c1 * r);
+        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = not_coincident(omc);
+        const double v = kernel(safe_omc(ok, omc), tab);
         acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
     }
 };
+using OpSal = OpSalT<false>;
+using OpSalLog = OpSalT<true>;
+
+// Calls f(op) with the device functor of a KernelSpec (kernel kind + SAL parameters).
+template <class KS, class F>
+void with_op(const KS& k, F&& f) {
+    switch (k.kind) {
+        case 0: f(OpLaplace{}); break;
+        case 1: f(OpBiharmonic{}); break;
+        case 2: f(OpBiotSavart{}); break;
+        default: {
+            const double pref = 3.0 * k.rho_ratio * kInv4Pi, c1 = 1.0 - k.b0, c2 = k.a1 - k.b1;
+            if (c1 != 0.0) f(OpSal::make(pref, c1, c2));
+            else f(OpSalLog::make(pref, c1, c2));
+        }
+    }
+}
 
 }  // namespace csfs_b200
