@@ -23,15 +23,9 @@ constexpr double kCoincidenceTol = 1e-14;  // kernels.hpp:28
 constexpr double kNodeTol = 1e-14;         // interpolation.cpp:8
 constexpr int kMaxDepth = 60;              // cluster_tree.cpp:11
 constexpr double kMinExtent = 1e-13;       // cluster_tree.cpp:12
-#ifndef CSFS_LOG_BITS
-#define CSFS_LOG_BITS 9
-#endif
-#ifndef CSFS_LOG_PACK
-#define CSFS_LOG_PACK 1
-#endif
-constexpr int kLogTabBits = CSFS_LOG_BITS;  // fastmath.cuh log table: 2^bits mantissa intervals
+constexpr int kLogTabBits = 9;             // fastmath.cuh log table: 512 mantissa intervals
 constexpr int kLogTab = 1 << kLogTabBits;
-constexpr int kLogTabWords = CSFS_LOG_PACK ? kLogTab : 2 * kLogTab;  // double2 words (global)
+constexpr int kLogTabWords = kLogTab;      // double2 words of the global table
 
 // Error classes that map onto the C-ABI return codes (include/csfs_b200.h).
 struct InvalidArgument : std::runtime_error {

@@ -2,16 +2,17 @@
 //
 // The evaluation phases are FP64-issue bound.  libdevice's log is
 // ~28 FP64 instructions, sqrt and a/b ~8 each; the kernel functors need:
-//   log   -> Tang-style table method: x = 2^e m, m r_i = 1 + t with |t| <= 2^-9 from a
-//            512-entry shared-memory table of 16-byte entries {L_hi_i, r_i | L_lo_i}:
-//            -ln r_i = L_hi + L_lo with L_hi a full double on the 2^-42 grid (so
-//            e ln2_hi + L_hi is exact) while r_i and L_lo carry 21 significant bits and are
-//            stored as the high words of doubles (the low words are zero): one LDS.128 per
-//            lookup.  log1p(t) by a degree-6 polynomial.  The two intervals touching
-//            x = 1 use r = 1 and r = 1/2 exactly, so t is exact and the result keeps full
-//            relative accuracy where log(x) ~ 0 — branch-free.  12 FP64 instructions
-//            (+ one int->double conversion on the XU pipe), <= 1 ulp (mpmath check in
-//            tests/test_gpu_numerics.py).
+//   log   -> Tang-style table method with an accurate table (Gal): x = 2^k m with
+//            m in [0.7070, 1.4141) (so both sides of x = 1 have k = 0), m r_i = 1 + t,
+//            |t| <= 2^-9, from a 512-entry shared-memory table of {r_i, L_i}: r_i is chosen
+//            near 1/centre_i so that L_i = -ln r_i is within 2^-67 of the 2^-46 grid
+//            (tools/gen_log_table.c), hence k ln2_hi + L_i is exact in one FMA and no
+//            low-order table word is needed: one conflict-prone LDS.128 per lookup, no
+//            register-pair assembly.  The two intervals around 1 use r = 1, L = 0, so
+//            t = m - 1 is exact and log keeps full relative accuracy where log(x) ~ 0 —
+//            branch-free.  log1p(t) by a degree-6 polynomial.  10 FP64 instructions (+ one
+//            int->double conversion on the XU pipe), <= 1 ulp (mpmath check in
+//            tests/test_gpu_numerics.py).  Domain: positive normals.
 //   rsqrt -> MUFU.RSQ64H seed + one cubic-convergent correction (5 FP64), <= 2 ulp.
 //   rcp   -> MUFU.RCP64H seed + one cubic-convergent correction (3 FP64), <= 2 ulp.
 // Arguments are finite positive normals (the coincidence guard keeps 1 - x.y >= 1e-14).
@@ -21,70 +22,44 @@
 
 namespace csfs_b200 {
 
-// Global table (host-built by make_log_table, kLogTab double2): .x = L_hi_i, .y = the
-// 64-bit word {hi: high word of r_i, lo: high word of L_lo_i}.  Staged into shared memory
-// per CTA.
+// Global table (host-built by make_log_table from log_table.inc): kLogTab double2 {r_i, L_i}.
+// Staged into shared memory per CTA.
 struct LogTable {
     const double2* e;  // kLogTab
-#if !CSFS_LOG_PACK
-    const double* lo;  // kLogTab
-#endif
 };
 
 struct LogTableSmem {
     double2 e[kLogTab];
-#if !CSFS_LOG_PACK
-    double lo[kLogTab];
-#endif
 };
 
 // Copies the global table into shared memory; the caller syncs before use.
 __device__ __forceinline__ LogTable stage_log_table(LogTableSmem& sm, const double2* g) {
-#if CSFS_LOG_PACK
     for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) sm.e[i] = g[i];
     return LogTable{sm.e};
-#else
-    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) {
-        sm.e[i] = g[i];
-        sm.lo[i] = g[kLogTab + i].x;
-    }
-    return LogTable{sm.e, sm.lo};
-#endif
 }
 
-constexpr double kLn2Hi = 0x1.62e42fefa3800p-1;  // 42 significant bits: e*kLn2Hi exact
-constexpr double kLn2Lo = 0x1.ef358p-45;         // ln 2 - kLn2Hi to 21 bits (|err| < 2^-66)
+constexpr int kLogOff = 0x3fe6a000;              // high word of the lowest m (~0.70703)
+constexpr double kLn2Hi = 0x1.62e42fefa3800p-1;  // 42 significant bits: k*kLn2Hi exact
+constexpr double kLn2Lo = 0x1.ef35793c76730p-45;
 
 __device__ __forceinline__ double fast_log(double x, const LogTable& tb) {
     const int hi = __double2hiint(x);
-    const int lo = __double2loint(x);
-    const int e = ((hi >> 20) & 0x7ff) - 1023;
-    const int i = (hi >> (20 - kLogTabBits)) & (kLogTab - 1);
-    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-    const double2 ent = tb.e[i];
-#if CSFS_LOG_PACK
-    const double r = __hiloint2double(__double2hiint(ent.y), 0);
-    const double L_lo = __hiloint2double(__double2loint(ent.y), 0);
-#else
-    const double r = ent.y, L_lo = tb.lo[i];
-#endif
-    // |t| <= 2^-9; exact for the two intervals touching x = 1 (r = 1 and r = 1/2)
-    const double t = fma(m, r, -1.0);
-#if CSFS_LOG_BITS >= 9
+    const int d = hi - kLogOff;
+    const int k = d >> 20;  // arithmetic shift: x = 2^k m, m in [0.7070, 1.4141)
+    const int i = (d >> (20 - kLogTabBits)) & (kLogTab - 1);
+    const double m = __hiloint2double(hi - (k << 20), __double2loint(x));
+    const double2 e = tb.e[i];
+    // |t| <= 2^-9; exact for the two intervals around m = 1 (r = 1)
+    const double t = fma(m, e.x, -1.0);
     double p = -1.0 / 6.0;
-#else
-    double p = 1.0 / 7.0;
-    p = fma(p, t, -1.0 / 6.0);
-#endif
     p = fma(p, t, 1.0 / 5.0);
     p = fma(p, t, -1.0 / 4.0);
     p = fma(p, t, 1.0 / 3.0);
     p = fma(p, t, -1.0 / 2.0);
-    const double ed = double(e);
-    const double small = fma(ed, kLn2Lo, L_lo);
-    const double q = fma(t * t, p, small);
-    const double A = fma(ed, kLn2Hi, ent.x);  // exact: both are multiples of 2^-42
-    return A + (t + q);
+    const double kd = double(k);
+    const double A = fma(kd, kLn2Hi, e.y);  // exact: multiples of 2^-46, |A| < 128
+    const double B = fma(kd, kLn2Lo, t);    // == t where k == 0
+    return A + fma(t * t, p, B);
 }
 
 __device__ __forceinline__ double rsqrt_seed(double x) {

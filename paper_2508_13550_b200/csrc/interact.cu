@@ -17,52 +17,19 @@
 // This is FP64-pipe bound: the inner loop is the kernel functor.
 #include <algorithm>
 #include <cmath>
-#include <cstring>
 
 #include "engine.hpp"
 #include "kernels_dev.cuh"
 
 namespace csfs_b200 {
 
-// fastmath.cuh table: r_i ~ 1/(1 + (i + 1/2)/kLogTab) rounded to 21 significant bits,
-// except r_0 = 1 (m in [1, 1 + 2^-9)) and r_last = 1/2 (m in [2 - 2^-9, 2)), where m r - 1
-// is exact; -ln r_i (of the rounded r_i, from long-double logl: 64-bit mantissa) =
-// L_hi + L_lo with L_hi on the 2^-42 grid (exact sums with e*ln2_hi) and L_lo rounded to
-// 21 bits (|err| <= 2^-64).  The r = 1/2 entry holds exactly the device's split of ln 2, so
-// e*ln2 + L cancels exactly at e = -1.
-static double round_hi_word(double v) {  // v rounded to the 21 significant bits of its high word
-    if (v == 0.0) return 0.0;
-    int ex = 0;
-    const double f = std::frexp(v, &ex);  // v = f 2^ex, |f| in [1/2, 1)
-    return std::ldexp(std::nearbyint(std::ldexp(f, 21)), ex - 21);
-}
-
+// fastmath.cuh table: {r_i, L_i} from tools/gen_log_table.c (verified by
+// tests/test_host.py::test_log_table).
 void make_log_table(double2* tab) {
-    for (int i = 0; i < kLogTab; ++i) {
-        double r = round_hi_word(1.0 / (1.0 + (i + 0.5) / kLogTab));
-        if (i == 0) r = 1.0;
-        if (i == kLogTab - 1) r = 0.5;
-        const long double L = -logl((long double)r);
-        double hi = double(nearbyintl(L * 0x1p42L) / 0x1p42L);
-        double lo = round_hi_word(double(L - (long double)hi));
-        if (i == 0) hi = lo = 0.0;
-        if (i == kLogTab - 1) {
-            hi = kLn2Hi;
-            lo = kLn2Lo;
-        }
-#if CSFS_LOG_PACK
-        unsigned long long rb, lb;
-        std::memcpy(&rb, &r, 8);
-        std::memcpy(&lb, &lo, 8);
-        const unsigned long long w = (rb & 0xffffffff00000000ull) | (lb >> 32);
-        double wd;
-        std::memcpy(&wd, &w, 8);
-        tab[i] = make_double2(hi, wd);
-#else
-        tab[i] = make_double2(hi, r);
-        tab[kLogTab + i] = make_double2(lo, 0.0);
-#endif
-    }
+    static const double kTab[kLogTab][2] = {
+#include "log_table.inc"
+    };
+    for (int i = 0; i < kLogTab; ++i) tab[i] = make_double2(kTab[i][0], kTab[i][1]);
 }
 
 namespace {
