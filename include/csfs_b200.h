@@ -125,6 +125,20 @@ CSFS_B200_API int csfs_b200_bve_step_device(csfs_b200_ctx* ctx, double* xyz, dou
                                             const csfs_b200_config* config, csfs_b200_stats* stage_stats,
                                             void* stream);
 
+/* --- barotropic vorticity: remesh (applications.hpp:91-94, applications.cpp:329-371) ------
+ * bve_remesh(state, neighbors): for every grid centre g_i, the k = min(max(neighbors, 6), n)
+ * nearest particles (lat-lon buckets, rings until >= k candidates then one more ring;
+ * ties by index), a Gaussian-weighted least-squares quadratic in g_i's face-local
+ * (xi, eta) over the usable ones (face_plane_coords), evaluated at g_i; fewer than 6
+ * usable neighbours -> the nearest particle's value.  Then xyz <- grid_xyz and zeta
+ * (n) / tracer (n, NULL: no tracer) <- the fitted values.  The reference's bve_step calls
+ * it after the RK4 update when BveStepOptions::remesh (default true, 12 neighbours).
+ * neighbors > 64 -> code 1 (a device-side limit of this library). */
+CSFS_B200_API int csfs_b200_bve_remesh(csfs_b200_ctx* ctx, double* xyz, double* zeta, double* tracer,
+                                       const double* grid_xyz, size_t n, int neighbors);
+CSFS_B200_API int csfs_b200_bve_remesh_device(csfs_b200_ctx* ctx, double* xyz, double* zeta, double* tracer,
+                                              const double* grid_xyz, size_t n, int neighbors, void* stream);
+
 /* --- stepwise state of the LAST csfmm call (parity / inspection) ------------------------
  * which: 0 target tree, 1 source tree.  Cluster ids are the REFERENCE's ids
  * (LIFO expansion order, cluster_tree.cpp:87-140). */

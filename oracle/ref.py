@@ -49,6 +49,8 @@ def lib() -> C.CDLL:
         L.csref_sph_harm_many.argtypes = [I, I, P, S, P]
         L.csref_rh_zeta_many.argtypes = [P, S, P]
         L.csref_bve_step.argtypes = [P, P, P, S, D, D, D, I, I, I]
+        L.csref_bve_remesh.argtypes = [P, P, P, P, S, I]
+        L.csref_bve_step_remesh.argtypes = [P, P, P, P, P, S, D, D, D, I, I, I, I]
         _lib = L
     return _lib
 
@@ -175,3 +177,30 @@ def bve_step(xyz, zeta, areas, omega, dt, mac=0.7, degree=6, n0=-1, threads=0):
     if rc:
         raise RuntimeError(lib().csref_last_error().decode())
     return xyz, zeta
+
+
+def bve_remesh(xyz, zeta, grid, tracer=None, neighbors=12):
+    """The reference's bve_remesh (applications.cpp:329-371): returns (grid, zeta', tracer')."""
+    xyz = np.array(xyz, dtype=np.float64, order="C")
+    zeta = np.array(zeta, dtype=np.float64)
+    tr = None if tracer is None else np.array(tracer, dtype=np.float64)
+    grid = np.ascontiguousarray(grid, dtype=np.float64)
+    rc = lib().csref_bve_remesh(_p(xyz), _p(zeta), _p(tr), _p(grid), xyz.shape[0], neighbors)
+    if rc:
+        raise RuntimeError(lib().csref_last_error().decode())
+    return xyz, zeta, tr
+
+
+def bve_step_remesh(xyz, zeta, areas, grid, omega, dt, tracer=None, mac=0.7, degree=6, n0=-1, neighbors=12,
+                    threads=0):
+    """The reference's bve_step with remesh on (its default BveStepOptions)."""
+    xyz = np.array(xyz, dtype=np.float64, order="C")
+    zeta = np.array(zeta, dtype=np.float64)
+    tr = None if tracer is None else np.array(tracer, dtype=np.float64)
+    areas = np.ascontiguousarray(areas, dtype=np.float64)
+    grid = np.ascontiguousarray(grid, dtype=np.float64)
+    rc = lib().csref_bve_step_remesh(_p(xyz), _p(zeta), _p(tr), _p(areas), _p(grid), xyz.shape[0], omega, dt, mac,
+                                     degree, n0, neighbors, threads)
+    if rc:
+        raise RuntimeError(lib().csref_last_error().decode())
+    return xyz, zeta, tr

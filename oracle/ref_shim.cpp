@@ -301,4 +301,55 @@ int csref_bve_step(double* xyz, double* zeta, const double* areas, size_t n, dou
     });
 }
 
+// bve_remesh (applications.cpp:329-371): positions <- grid, zeta/tracer <- the LSQ fits.
+int csref_bve_remesh(double* xyz, double* zeta, double* tracer, const double* grid, size_t n, int neighbors) {
+    return guarded([&] {
+        BveState s;
+        s.positions = to_vec3(xyz, n);
+        s.zeta.assign(zeta, zeta + n);
+        if (tracer) s.tracer.assign(tracer, tracer + n);
+        s.grid_centers = to_vec3(grid, n);
+        s.areas.assign(n, 0.0);
+        bve_remesh(s, neighbors);
+        for (size_t i = 0; i < n; ++i) {
+            xyz[3 * i] = s.positions[i].x;
+            xyz[3 * i + 1] = s.positions[i].y;
+            xyz[3 * i + 2] = s.positions[i].z;
+            zeta[i] = s.zeta[i];
+            if (tracer) tracer[i] = s.tracer[i];
+        }
+    });
+}
+
+// bve_step with BveStepOptions::remesh on (the reference's default): RK4 then remesh onto
+// grid (n x 3).
+int csref_bve_step_remesh(double* xyz, double* zeta, double* tracer, const double* areas, const double* grid,
+                          size_t n, double omega, double dt, double mac, int degree, int n0, int neighbors,
+                          int threads) {
+    return guarded([&] {
+        BveState s;
+        s.positions = to_vec3(xyz, n);
+        s.zeta.assign(zeta, zeta + n);
+        if (tracer) s.tracer.assign(tracer, tracer + n);
+        s.areas.assign(areas, areas + n);
+        s.grid_centers = to_vec3(grid, n);
+        s.omega = omega;
+        BveStepOptions o;
+        o.traversal.mac = mac;
+        o.traversal.degree = degree;
+        o.traversal.n0 = n0;
+        o.traversal.threads = threads;
+        o.remesh = true;
+        o.remesh_neighbors = neighbors;
+        bve_step(s, dt, o);
+        for (size_t i = 0; i < n; ++i) {
+            xyz[3 * i] = s.positions[i].x;
+            xyz[3 * i + 1] = s.positions[i].y;
+            xyz[3 * i + 2] = s.positions[i].z;
+            zeta[i] = s.zeta[i];
+            if (tracer) tracer[i] = s.tracer[i];
+        }
+    });
+}
+
 }  // extern "C"

@@ -2,6 +2,8 @@
 (csfs::csfmm_sum, /root/reference/proj/src/summation.cpp:383-421) as hand-written CUDA
 behind a C-ABI (include/csfs_b200.h)."""
 from .engine import (  # noqa: F401
+    BveState,
+    BveStepOptions,
     Engine,
     Kernel,
     KernelKind,
@@ -11,6 +13,8 @@ from .engine import (  # noqa: F401
     SalParams,
     SumStats,
     TraversalConfig,
+    bve_remesh,
+    bve_step,
     csfmm_sum,
     default_engine,
     direct_sum,

@@ -33,6 +33,8 @@ struct csfs_b200_ctx {
     DevBuf<int2> d_segs;
     DevBuf<double2> log_tab;  // fastmath.cuh table, uploaded once per context
     DevBuf<double> bve;       // RK4 stage buffers (csfs_b200_bve_step)
+    DevBuf<int> rm_i;         // remesh buckets (csfs_b200_bve_remesh)
+    DevBuf<double> rm_d, rm_h;
     cudaEvent_t ev[8] = {};
     Cheb cheb{};
     KernelSpec kspec;
@@ -590,6 +592,48 @@ int csfs_b200_bve_step(csfs_b200_ctx* c, double* xyz, double* zeta, const double
         if (rc != CSFS_B200_OK) throw CudaFailure(c->err);
         CSFS_CK(cudaMemcpyAsync(xyz, c->h_txyz.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaMemcpyAsync(zeta, c->h_w.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
+    });
+}
+
+// --- BVE remesh (applications.cpp:329-371) -----------------------------------------------
+
+namespace {
+void check_remesh(int neighbors) {
+    if (neighbors > kRemeshMaxK)
+        throw InvalidArgument("remesh_neighbors above " + std::to_string(kRemeshMaxK) + " is not supported");
+}
+}  // namespace
+
+int csfs_b200_bve_remesh_device(csfs_b200_ctx* c, double* xyz, double* zeta, double* tracer,
+                                const double* grid_xyz, size_t n, int neighbors, void* stream) {
+    return guarded(c, [&] {
+        check_remesh(neighbors);
+        cudaStream_t s = pick(c, stream);
+        bve_remesh(xyz, zeta, tracer, grid_xyz, (long long)n, neighbors, c->rm_i, c->rm_d, s);
+        CSFS_CK(cudaStreamSynchronize(s));
+    });
+}
+
+int csfs_b200_bve_remesh(csfs_b200_ctx* c, double* xyz, double* zeta, double* tracer, const double* grid_xyz,
+                         size_t n, int neighbors) {
+    return guarded(c, [&] {
+        check_remesh(neighbors);
+        if (n == 0) return;
+        cudaStream_t s = c->own;
+        c->rm_h.grow(n * (tracer ? 8 : 7));
+        double* dx = c->rm_h.p;
+        double* dg = dx + 3 * n;
+        double* dz = dg + 3 * n;
+        double* dt = tracer ? dz + n : nullptr;
+        CSFS_CK(cudaMemcpyAsync(dx, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        CSFS_CK(cudaMemcpyAsync(dg, grid_xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        CSFS_CK(cudaMemcpyAsync(dz, zeta, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        if (tracer) CSFS_CK(cudaMemcpyAsync(dt, tracer, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        bve_remesh(dx, dz, dt, dg, (long long)n, neighbors, c->rm_i, c->rm_d, s);
+        CSFS_CK(cudaMemcpyAsync(xyz, dx, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaMemcpyAsync(zeta, dz, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (tracer) CSFS_CK(cudaMemcpyAsync(tracer, dt, n * sizeof(double), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaStreamSynchronize(s));
     });
 }

@@ -212,6 +212,12 @@ void cstc_eval(const KernelSpec& k, const double* txyz, long long nt, const int*
                double mac, int n0, const double2* log_tab, double* out, unsigned long long* counts,
                cudaStream_t s);
 
+// remesh.cu: bve_remesh (applications.cpp:329-371) on the device; at most kRemeshMaxK
+// neighbours per grid centre.  xyz <- grid, zeta/tracer (tracer may be null) <- the fits.
+constexpr int kRemeshMaxK = 64;
+void bve_remesh(double* xyz, double* zeta, double* tracer, const double* grid, long long n, int neighbors,
+                DevBuf<int>& ibuf, DevBuf<double>& dbuf, cudaStream_t s);
+
 // bve.cu: RK4 stage arithmetic of bve_step (applications.cpp:378-412)
 void bve_weights(long long n, const double* zeta, const double* area, double* w, cudaStream_t s);
 void bve_advance(long long n, const double* x0, const double* z0, const double* k, double h, double omega,

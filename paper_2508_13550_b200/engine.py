@@ -162,6 +162,8 @@ def lib() -> C.CDLL:
                                          C.POINTER(SumStats)]
         L.csfs_b200_bve_step_device.argtypes = [P, P, P, P, S, C.c_double, C.c_double, C.POINTER(_CConfig),
                                                 C.POINTER(SumStats), P]
+        L.csfs_b200_bve_remesh.argtypes = [P, P, P, P, P, S, I]
+        L.csfs_b200_bve_remesh_device.argtypes = [P, P, P, P, P, S, I, P]
         L.csfs_b200_eval_pairs.argtypes = [P, C.POINTER(_CKernel), P, P, S, P]
         L.csfs_b200_eval_math.argtypes = [P, I, P, S, P]
         L.csfs_b200_part_sizes.argtypes = [P, C.POINTER(S), C.POINTER(S)]
@@ -348,6 +350,25 @@ class Engine:
         return list(st)
 
     # --- multi-GPU partition phases (see distributed.py) ------------------------------
+    def bve_remesh(self, xyz: np.ndarray, zeta: np.ndarray, grid: np.ndarray, tracer: np.ndarray | None = None,
+                   neighbors: int = 12) -> tuple[np.ndarray, np.ndarray, np.ndarray | None]:
+        """bve_remesh (applications.cpp:329-371) on the GPU: returns (positions = grid copy,
+        fitted zeta, fitted tracer or None); inputs untouched."""
+        x = np.array(xyz, dtype=np.float64, order="C", copy=True)
+        z = np.array(zeta, dtype=np.float64, copy=True)
+        t = None if tracer is None else np.array(tracer, dtype=np.float64, copy=True)
+        g = np.ascontiguousarray(grid, dtype=np.float64)
+        if g.shape != x.shape or z.shape[0] != x.shape[0] or (t is not None and t.shape[0] != x.shape[0]):
+            raise ValueError("positions, zeta, tracer and grid centres must have one entry per particle")
+        self._check(self._lib.csfs_b200_bve_remesh(self._h, _ptr(x), _ptr(z), _ptr(t) if t is not None else None,
+                                                   _ptr(g), x.shape[0], int(neighbors)))
+        return x, z, t
+
+    def bve_remesh_device(self, xyz, zeta, tracer, grid, n: int, neighbors: int = 12, stream: int = 0):
+        self._check(self._lib.csfs_b200_bve_remesh_device(self._h, _dptr(xyz), _dptr(zeta),
+                                                          _dptr(tracer) if tracer is not None else None,
+                                                          _dptr(grid), n, int(neighbors), C.c_void_p(stream)))
+
     def part_plan(self, tgt_xyz, nt, src_xyz, src_w, ns, kernel, config, stream=0):
         """Arguments are device tensors or raw device addresses."""
         self._check(self._lib.csfs_b200_part_plan(
@@ -431,3 +452,42 @@ def direct_sum(targets, sources, kernel, threads=0) -> PotentialField:
 
 def summed_potential(targets, sources, kernel, config, stats=None) -> PotentialField:
     return default_engine().summed_potential(targets, sources, kernel, config, stats)
+
+
+@dataclass
+class BveState:  # applications.hpp:58-66
+    positions: np.ndarray  # n x 3
+    zeta: np.ndarray
+    areas: np.ndarray
+    grid_centers: np.ndarray
+    tracer: np.ndarray | None = None
+    omega: float = 2.0 * np.pi
+    time: float = 0.0
+
+
+@dataclass
+class BveStepOptions:  # applications.hpp:79-83
+    traversal: TraversalConfig = field(default_factory=TraversalConfig)
+    remesh: bool = True
+    remesh_neighbors: int = 12
+
+
+def bve_remesh(state: BveState, neighbors: int = 12, engine: Engine | None = None) -> None:
+    """applications.hpp:94: positions return to the grid centres, zeta/tracer are refitted."""
+    e = engine or default_engine()
+    state.positions, state.zeta, state.tracer = e.bve_remesh(state.positions, state.zeta, state.grid_centers,
+                                                             state.tracer, neighbors)
+
+
+def bve_step(state: BveState, dt: float, options: BveStepOptions | None = None,
+             engine: Engine | None = None) -> list:
+    """applications.hpp:89 / applications.cpp:378-412: one RK4 step (4 Biot-Savart CSFMM sums
+    on the GPU), then the remesh when options.remesh.  Returns the per-stage SumStats."""
+    o = options or BveStepOptions()
+    e = engine or default_engine()
+    state.positions, state.zeta, st = e.bve_step(state.positions, state.zeta, state.areas, state.omega, dt,
+                                                 o.traversal)
+    state.time += dt
+    if o.remesh:
+        bve_remesh(state, o.remesh_neighbors, e)
+    return st

@@ -70,3 +70,74 @@ def test_bve_rejects_nonpositive_dt(engine):
     wl = configs.make("c4", level=3)
     with pytest.raises(ValueError, match="time step must be positive"):
         engine.bve_step(wl.xyz, wl.f, wl.areas, 1.0, 0.0, TraversalConfig())
+
+
+def deformed_state(level, steps=3, dt=0.05):
+    """Particles advected by the reference's own RK4 steps (remesh off): a genuinely
+    scattered set for the remesh (neighbour sets cross faces and bucket rings)."""
+    wl = configs.make("c4", level=level)
+    x, z = wl.xyz, wl.f
+    for _ in range(steps):
+        x, z = ref.bve_step(x, z, wl.areas, wl.meta["omega_per_day"], dt, mac=wl.mac, degree=wl.degree, n0=wl.n0)
+    return wl, x, z
+
+
+@pytest.mark.parametrize("level,neighbors", [(5, 12), (7, 12), (7, 20), (6, 6)])
+def test_remesh_matches_reference(engine, level, neighbors):
+    """Same neighbour sets, stencils and pivots as the reference; the values agree to the
+    conditioning of the 6x6 normal equations.  That conditioning is measured here: the
+    reference's own result moves by `sens` when the particle positions move by 1 ulp
+    (libdevice vs glibc atan/exp/acos differ by ~1 ulp), and ours must sit within it."""
+    wl, x, z = deformed_state(level)
+    tracer = np.cos(3 * wl.xyz[:, 0]) * np.sin(2 * wl.xyz[:, 2])
+    gx, gz, gt = engine.bve_remesh(x, z, wl.xyz, tracer=tracer, neighbors=neighbors)
+    rx, rz, rt = ref.bve_remesh(x, z, wl.xyz, tracer=tracer, neighbors=neighbors)
+    np.testing.assert_array_equal(gx, rx)  # positions return to the grid centres exactly
+    ulp = np.random.default_rng(level).choice([-1.0, 1.0], size=x.shape) * 2.0 ** -52
+    _, pz, pt = ref.bve_remesh(x * (1 + ulp), z, wl.xyz, tracer=tracer, neighbors=neighbors)
+    sens_z, sens_t = rel_l2(pz, rz), rel_l2(pt, rt)
+    assert rel_l2(gz, rz) <= max(1e-13, 3 * sens_z)
+    assert rel_l2(gt, rt) <= max(1e-13, 3 * sens_t)
+    if neighbors >= 12:  # over-determined fits: well inside 1e-9 (k = 6 interpolates: ~1e-6)
+        assert rel_l2(gz, rz) < 1e-9 and rel_l2(gt, rt) < 1e-9
+    # pointwise: no point off by more than the reference's own 1-ulp response allows
+    assert np.max(np.abs(gz - rz)) <= max(1e-12, 10 * np.max(np.abs(pz - rz)))
+
+
+def test_remesh_edge_cases(engine):
+    rng = np.random.default_rng(5)
+    p = rng.normal(size=(40, 3))
+    p /= np.linalg.norm(p, axis=1, keepdims=True)
+    g = rng.normal(size=(40, 3))
+    g /= np.linalg.norm(g, axis=1, keepdims=True)
+    z = rng.normal(size=40)
+    for n in (1, 3, 5, 6, 7, 40):  # k = min(max(neighbors, 6), n): fewer than 6 -> nearest value
+        for nb in (1, 12):
+            gx, gz, _ = engine.bve_remesh(p[:n], z[:n], g[:n], neighbors=nb)
+            rx, rz, _ = ref.bve_remesh(p[:n], z[:n], g[:n], neighbors=nb)
+            np.testing.assert_array_equal(gx, rx)
+            np.testing.assert_allclose(gz, rz, rtol=1e-9, atol=1e-12)
+    gx, gz, gt = engine.bve_remesh(np.zeros((0, 3)), np.zeros(0), np.zeros((0, 3)))
+    assert gx.shape == (0, 3) and gz.shape == (0,) and gt is None
+    with pytest.raises(ValueError, match="remesh_neighbors above 64"):
+        engine.bve_remesh(p, z, g, neighbors=65)
+
+
+def test_bve_step_with_remesh_matches_reference(engine):
+    """The reference's default BveStepOptions (remesh on, 12 neighbours): RK4 + remesh."""
+    from paper_2508_13550_b200 import BveState, BveStepOptions, bve_step
+
+    wl = configs.make("c4", level=6)
+    tracer = wl.xyz[:, 2].copy()
+    cfg = TraversalConfig(mac=wl.mac, degree=wl.degree, n0=wl.n0)
+    st = BveState(positions=wl.xyz.copy(), zeta=wl.f.copy(), areas=wl.areas, grid_centers=wl.xyz,
+                  tracer=tracer.copy(), omega=wl.meta["omega_per_day"])
+    for _ in range(2):
+        bve_step(st, 0.05, BveStepOptions(traversal=cfg), engine)
+    rx, rz, rt = wl.xyz, wl.f, tracer
+    for _ in range(2):
+        rx, rz, rt = ref.bve_step_remesh(rx, rz, wl.areas, wl.xyz, wl.meta["omega_per_day"], 0.05, tracer=rt,
+                                         mac=wl.mac, degree=wl.degree, n0=wl.n0)
+    np.testing.assert_array_equal(st.positions, rx)
+    assert rel_l2(st.zeta, rz) < 1e-9 and rel_l2(st.tracer, rt) < 1e-9  # remesh conditioning, see above
+    assert abs(st.time - 0.1) < 1e-15

@@ -122,3 +122,34 @@ def test_log_table():
         assert (Fraction(L) * 2 ** 46).denominator == 1
         assert abs(-mpmath.log(mpmath.mpf(r)) - mpmath.mpf(L)) < mpmath.mpf(2) ** -67
         assert max(abs(Fraction(lo) * Fraction(r) - 1), abs(Fraction(hi) * Fraction(r) - 1)) <= Fraction(1, 512)
+
+
+def test_bve_mirror_defaults_and_sequencing():
+    """BveState / BveStepOptions defaults (applications.hpp:58-83) and bve_step's order:
+    RK4 step, time += dt, then the remesh only when options.remesh."""
+    from paper_2508_13550_b200 import BveState, BveStepOptions, bve_step
+
+    o = BveStepOptions()
+    assert o.remesh is True and o.remesh_neighbors == 12 and o.traversal.mac == 0.7
+    calls = []
+
+    class Fake:
+        def bve_step(self, x, z, a, omega, dt, cfg):
+            calls.append(("step", dt, omega))
+            return x + 1.0, z + 1.0, ["stats"] * 4
+
+        def bve_remesh(self, x, z, g, t, nb):
+            calls.append(("remesh", nb))
+            return g.copy(), z * 2.0, t
+
+    g = np.zeros((3, 3))
+    st = BveState(positions=g + 0.5, zeta=np.ones(3), areas=np.ones(3), grid_centers=g)
+    assert st.omega == 2.0 * np.pi and st.tracer is None
+    bve_step(st, 0.25, BveStepOptions(remesh_neighbors=20), Fake())
+    assert calls == [("step", 0.25, 2.0 * np.pi), ("remesh", 20)]
+    np.testing.assert_array_equal(st.positions, g)
+    np.testing.assert_array_equal(st.zeta, 4.0)
+    assert st.time == 0.25
+    calls.clear()
+    bve_step(st, 0.25, BveStepOptions(remesh=False), Fake())
+    assert calls == [("step", 0.25, 2.0 * np.pi)] and st.time == 0.5
