@@ -76,6 +76,14 @@ int guarded(csfs_b200_ctx* c, F&& f) {
     }
 }
 
+// Re-raises a nested entry point's return code as the matching exception.
+void rethrow(csfs_b200_ctx* c, int rc) {
+    if (rc == CSFS_B200_OK) return;
+    if (rc == CSFS_B200_INVALID_ARGUMENT) throw InvalidArgument(c->err);
+    if (rc == CSFS_B200_OUT_OF_MEMORY) throw OutOfMemory(c->err);
+    throw CudaFailure(c->err);
+}
+
 KernelSpec to_spec(const csfs_b200_kernel* k) {
     if (!k) throw InvalidArgument("kernel must not be null");
     if (k->kind < 0 || k->kind > 3) throw InvalidArgument("unknown kernel kind: " + std::to_string(k->kind));
@@ -537,7 +545,7 @@ int csfs_b200_cstc(csfs_b200_ctx* c, const double* txyz, size_t nt, const double
         c->h_out.grow(std::max<size_t>(nout, 1));
         const int rc = csfs_b200_cstc_device(c, c->h_txyz.p, nt, dsrc, c->h_w.p, ns, k, cfg, c->h_out.p, st, s);
         if (rc == CSFS_B200_INVALID_ARGUMENT) throw InvalidArgument(c->err);
-        if (rc != CSFS_B200_OK) throw CudaFailure(c->err);
+        rethrow(c, rc);
         if (nout) CSFS_CK(cudaMemcpyAsync(out, c->h_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaStreamSynchronize(s));
     });
@@ -589,7 +597,7 @@ int csfs_b200_bve_step(csfs_b200_ctx* c, double* xyz, double* zeta, const double
         CSFS_CK(cudaMemcpyAsync(c->h_out.p, areas, n * sizeof(double), cudaMemcpyHostToDevice, s));
         const int rc = csfs_b200_bve_step_device(c, c->h_txyz.p, c->h_w.p, c->h_out.p, n, omega, dt, cfg,
                                                  stage_stats, s);
-        if (rc != CSFS_B200_OK) throw CudaFailure(c->err);
+        rethrow(c, rc);
         CSFS_CK(cudaMemcpyAsync(xyz, c->h_txyz.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaMemcpyAsync(zeta, c->h_w.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaStreamSynchronize(s));

@@ -1,5 +1,6 @@
-// C++ host shim: the reference's csfs::csfmm_sum / direct_sum signatures
-// (/root/reference/proj/include/csfs/summation.hpp:74-88) implemented on the B200 C-ABI
+// C++ host shim: the reference's csfs::csfmm_sum / cstc_sum / direct_sum / summed_potential
+// signatures (/root/reference/proj/include/csfs/summation.hpp:74-88) and the BVE driver's
+// bve_step / bve_remesh (applications.hpp:89-94) implemented on the B200 C-ABI
 // (include/csfs_b200.h).  A maintainer compiles this file against the reference's headers
 // and links libcsfs_b200.so in place of summation.cpp's csfmm_sum.
 // CSFS_B200_SHIM_NAMESPACE lets the tests build it side by side with the reference
@@ -7,6 +8,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "csfs/applications.hpp"
 #include "csfs/summation.hpp"
 #include "csfs_b200.h"
 
@@ -149,6 +151,33 @@ csfs::PotentialField summed_potential(const csfs::ParticleSet& targets, const cs
         case csfs::Method::Cstc: return CSFS_B200_SHIM_NAMESPACE::cstc_sum(targets, sources, kernel, config, stats);
         default: return CSFS_B200_SHIM_NAMESPACE::csfmm_sum(targets, sources, kernel, config, stats);
     }
+}
+
+}  // namespace CSFS_B200_SHIM_NAMESPACE
+
+namespace CSFS_B200_SHIM_NAMESPACE {
+
+// bve_remesh (applications.hpp:94, applications.cpp:329-371)
+void bve_remesh(csfs::BveState& state, int neighbors) {
+    const size_t n = state.positions.size();
+    if (state.zeta.size() != n || state.grid_centers.size() != n || (!state.tracer.empty() && state.tracer.size() != n))
+        throw std::invalid_argument("positions, zeta, tracer and grid centres must have one entry per particle");
+    if (n == 0) return;
+    check(csfs_b200_bve_remesh(thread_ctx(), &state.positions[0].x, state.zeta.data(),
+                               state.tracer.empty() ? nullptr : state.tracer.data(), &state.grid_centers[0].x, n,
+                               neighbors));
+}
+
+// bve_step (applications.hpp:89, applications.cpp:378-412): RK4 on the device, then the
+// remesh when options.remesh.
+void bve_step(csfs::BveState& state, double dt, const csfs::BveStepOptions& options) {
+    const csfs::TraversalConfig& t = options.traversal;
+    const csfs_b200_config c{t.mac, t.degree, t.n0, t.shrink ? 1 : 0};
+    check(csfs_b200_bve_step(thread_ctx(), state.positions.empty() ? nullptr : &state.positions[0].x,
+                             state.zeta.data(), state.areas.data(), state.positions.size(), state.omega, dt, &c,
+                             nullptr));
+    state.time += dt;
+    if (options.remesh) CSFS_B200_SHIM_NAMESPACE::bve_remesh(state, options.remesh_neighbors);
 }
 
 }  // namespace CSFS_B200_SHIM_NAMESPACE

@@ -2,6 +2,7 @@
 // the reference's own headers and types, against the reference library's csfs::csfmm_sum /
 // direct_sum on the reference's own grids and weights — the drop-in exercised from C++.
 // Prints one line per case: name rel_l2 pp pc cp cc (GPU) pp pc cp cc (reference).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
@@ -15,6 +16,7 @@ csfs::PotentialField csfmm_sum(const csfs::ParticleSet&, const csfs::ParticleSet
 csfs::PotentialField direct_sum(const csfs::ParticleSet&, const csfs::ParticleSet&, const csfs::Kernel&, int);
 csfs::PotentialField summed_potential(const csfs::ParticleSet&, const csfs::ParticleSet&, const csfs::Kernel&,
                                       const csfs::TraversalConfig&, csfs::SumStats*);
+void bve_step(csfs::BveState&, double, const csfs::BveStepOptions&);
 }  // namespace csfs_gpu
 
 using namespace csfs;
@@ -81,6 +83,24 @@ int main() {
                                 csfs::summed_potential(p, p, Kernel::parse("sal"), cfg, &sr));
         std::printf("cstc_sal %.3e %zu %zu | %zu %zu\n", e, sg.pp, sg.pc, sr.pp, sr.pc);
         if (!(e < 1e-10) || sg.pp != sr.pp || sg.pc != sr.pc) ++bad;
+    }
+    {  // bve_step with the reference's default options (remesh on, 12 neighbours), with a tracer
+        const SphericalGrid g = build_grid(GridKind::CubedSphere, 4);
+        BveState a = bve_initial(BveInit::RossbyHaurwitz, g, true), b = a;
+        BveStepOptions o;
+        o.traversal.degree = 6;
+        o.traversal.mac = 0.7;
+        csfs_gpu::bve_step(a, 0.05, o);
+        bve_step(b, 0.05, o);
+        double num = 0, den = 0, pos = 0;
+        for (size_t i = 0; i < a.zeta.size(); ++i) {
+            num += (a.zeta[i] - b.zeta[i]) * (a.zeta[i] - b.zeta[i]) + (a.tracer[i] - b.tracer[i]) * (a.tracer[i] - b.tracer[i]);
+            den += b.zeta[i] * b.zeta[i] + b.tracer[i] * b.tracer[i];
+            pos = std::max(pos, std::fabs(a.positions[i].x - b.positions[i].x));
+        }
+        const double e = std::sqrt(num / den);
+        std::printf("bve_step_remesh %.3e pos %.1e time %g %g\n", e, pos, a.time, b.time);
+        if (!(e < 1e-9) || pos != 0.0 || a.time != b.time) ++bad;
     }
     {  // the reference's exception contract
         ParticleSet empty, one;
