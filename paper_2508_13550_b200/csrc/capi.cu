@@ -40,6 +40,7 @@ struct csfs_b200_ctx {
     KernelSpec kspec;
     FmmConfig cfg;
     bool have_state = false;
+    bool have_src_tree = false;  // the last call was cstc: only the source tree exists
     int dim = 1;
     bool use_mutual = true;  // symmetric PP evaluation (CSFS_B200_NO_SYMMETRIC=1 disables)
     // multi-GPU partition state (csfs_b200_part_*)
@@ -160,6 +161,7 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
                csfs_b200_stats* st, cudaStream_t s) {
     validate(f, nt, ns);
     c->have_state = false;
+    c->have_src_tree = false;
     c->kspec = ks;
     c->cfg = f;
     c->dim = ks.out_dim();
@@ -260,8 +262,9 @@ HostTree fetch_topology(const DeviceTree& t) {
 }
 
 const DeviceTree& which_tree(const csfs_b200_ctx* c, int which) {
-    if (!c->have_state) throw InvalidArgument("no csfmm state: call csfs_b200_csfmm first");
     if (which != 0 && which != 1) throw InvalidArgument("which must be 0 (target) or 1 (source)");
+    if (c->have_src_tree && which == 1) return c->stree;  // after cstc
+    if (!c->have_state) throw InvalidArgument("no csfmm state: call csfs_b200_csfmm first");
     return (which == 0 || c->shared) ? c->ttree : c->stree;
 }
 
@@ -387,8 +390,9 @@ int csfs_b200_direct(csfs_b200_ctx* c, const double* txyz, size_t nt, const doub
 
 int csfs_b200_tree_info(const csfs_b200_ctx* c, int which, int* ncl, int* depth, size_t* n, int* npp) {
     if (!c) return CSFS_B200_INVALID_ARGUMENT;
-    if (!c->have_state || (which != 0 && which != 1)) return CSFS_B200_INVALID_ARGUMENT;
-    const DeviceTree& t = (which == 0 || c->shared) ? c->ttree : c->stree;
+    const bool src_only = c->have_src_tree && which == 1;
+    if ((!c->have_state && !src_only) || (which != 0 && which != 1)) return CSFS_B200_INVALID_ARGUMENT;
+    const DeviceTree& t = src_only ? c->stree : (which == 0 || c->shared) ? c->ttree : c->stree;
     if (ncl) *ncl = t.ncl;
     if (depth) *depth = t.depth_max();
     if (n) *n = size_t(t.n);
@@ -491,6 +495,7 @@ int csfs_b200_cstc_device(csfs_b200_ctx* c, const double* txyz, size_t nt, const
         if (f.resolved_n0() < 1) throw InvalidArgument("maximum leaf size must be at least 1");
         cudaStream_t s = pick(c, stream);
         c->have_state = false;
+        c->have_src_tree = false;
         c->cheb = make_cheb(f.degree);
         const int n0 = f.resolved_n0();
         cudaEvent_t* ev = c->ev;
@@ -509,6 +514,7 @@ int csfs_b200_cstc_device(csfs_b200_ctx* c, const double* txyz, size_t nt, const
         CSFS_CK(cudaMemcpyAsync(cnt, c->items.pairs.p + 6, sizeof(cnt), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaEventSynchronize(ev[3]));
         CSFS_CK(cudaStreamSynchronize(s));
+        c->have_src_tree = true;
         if (st) {
             std::memset(st, 0, sizeof(*st));
             st->t_tree_build = ev_ms(ev[0], ev[1]) * 1e-3;
@@ -657,6 +663,7 @@ int csfs_b200_part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const d
         validate(f, nt, ns);
         cudaStream_t s = pick(c, stream);
         c->have_state = false;
+        c->have_src_tree = false;
         c->part_planned = false;
         c->part_stream = s;
         c->kspec = ks;

@@ -5,6 +5,7 @@
 // and links libcsfs_b200.so in place of summation.cpp's csfmm_sum.
 // CSFS_B200_SHIM_NAMESPACE lets the tests build it side by side with the reference
 // (tests/cpp/shim_parity.cpp) without a symbol clash.
+#include <chrono>
 #include <stdexcept>
 #include <string>
 
@@ -141,9 +142,12 @@ csfs::PotentialField summed_potential(const csfs::ParticleSet& targets, const cs
                                       csfs::SumStats* stats) {
     switch (config.method) {
         case csfs::Method::Direct: {
+            const auto t0 = std::chrono::steady_clock::now();
             csfs::PotentialField f = CSFS_B200_SHIM_NAMESPACE::direct_sum(targets, sources, kernel, config.threads);
             if (stats) {
                 *stats = csfs::SumStats{};
+                stats->t_traversal = stats->t_total =
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
                 stats->pp = targets.size() * sources.size();
             }
             return f;
