@@ -43,6 +43,7 @@ struct csfs_b200_ctx {
     bool have_src_tree = false;  // the last call was cstc: only the source tree exists
     int dim = 1;
     bool use_mutual = true;  // symmetric PP evaluation (CSFS_B200_NO_SYMMETRIC=1 disables)
+    bool mutual_unit_scope = false;  // CSFS_B200_MUTUAL_SCOPE=unit: single-GPU pairs like the partitioned path
     // multi-GPU partition state (csfs_b200_part_*)
     bool part_planned = false;
     cudaStream_t part_stream = nullptr;
@@ -147,11 +148,16 @@ int count_internal(const DeviceTree& t) {
 }
 
 // Symmetric PP evaluation (targets == sources only): pairs within one partition unit.
-void prepare_mutual(csfs_b200_ctx* c, cudaStream_t s) {
+// Symmetric PP pairs (k_mutual).  Scope: one GPU pairs every mirrored leaf pair
+// (`global`); the partitioned multi-GPU path restricts them to pairs inside one partition
+// unit, so no pair straddles two ranks and every rank count sums in the same order
+// (results bitwise equal across rank counts; equal to the single-GPU result to rounding).
+void prepare_mutual(csfs_b200_ctx* c, cudaStream_t s, bool global) {
     c->items.mutual = false;
     if (!c->shared || !c->use_mutual || c->kspec.out_dim() != 1) return;
     std::vector<long long> ub, ue;
-    partition_units(c->ttree, ub, ue);
+    if (global && !c->mutual_unit_scope) ub.push_back(0);
+    else partition_units(c->ttree, ub, ue);
     build_mutual(c->ttree, c->items, ub, c->sc, s);
     c->items.mutual = c->items.n_partial > 0;
 }
@@ -183,7 +189,7 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
 
     dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
     build_items(T, S, c->lists, c->items, c->sc, s);
-    prepare_mutual(c, s);
+    prepare_mutual(c, s, true);
     CSFS_CK(cudaEventRecord(ev[3], s));
 
     const int dim = c->dim;
@@ -291,6 +297,8 @@ int csfs_b200_create(csfs_b200_ctx** out, int device) {
         CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
         const char* nosym = std::getenv("CSFS_B200_NO_SYMMETRIC");
         c->use_mutual = !(nosym && nosym[0] == '1');
+        const char* scope = std::getenv("CSFS_B200_MUTUAL_SCOPE");
+        c->mutual_unit_scope = scope && std::string(scope) == "unit";
         std::vector<double2> tab(kLogTabWords);
         make_log_table(tab.data());
         c->log_tab.grow(kLogTabWords);
@@ -678,7 +686,7 @@ int csfs_b200_part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const d
         if (!c->shared) build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s);
         dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
         build_items(T, S, c->lists, c->items, c->sc, s);
-        prepare_mutual(c, s);  // same choice as the single-GPU path: bitwise-equal results
+        prepare_mutual(c, s, false);  // unit scope: the same pairs for every rank count
         // partition units: depth-1 subtrees plus unsplit roots, in tree order
         for (int w = 0; w < 2; ++w) {
             const DeviceTree& t = (w == 0 || c->shared) ? T : S;

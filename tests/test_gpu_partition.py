@@ -1,8 +1,10 @@
 """Multi-GPU target partitioning on ONE GPU: the R ranks are emulated one after the other
 (each rank's phase is an independent launch; the all-reduces are done here on the device
 by summing the per-rank buffers), so nothing waits on another rank.  The result must be
-BITWISE identical to the single-GPU evaluation for every R (each target is evaluated by
-exactly one rank in the single-GPU order; every reduced slot has one non-zero term)."""
+BITWISE identical for every R (each target is evaluated by exactly one rank in a fixed
+order; every reduced slot has one non-zero term), and bitwise equal to the single-GPU
+csfmm run with the same symmetric-pair scope (CSFS_B200_MUTUAL_SCOPE=unit); the default
+single-GPU scope pairs more leaves symmetrically and agrees to rounding."""
 import numpy as np
 import pytest
 import torch
@@ -45,6 +47,10 @@ def test_partition_bitwise(engine, name, level, kname):
                         torch.cuda.current_stream().cuda_stream)
     want = ref_out.cpu().numpy()
     want_pw = engine.proxy_weights_export()
+    one, _, _ = emulate(engine, xyz, w, k, cfg, 1)
+    one = one.cpu().numpy()
+    assert np.sqrt(np.sum((one - want) ** 2) / np.sum(want ** 2)) < 1e-14  # global vs unit pair scope
+    want = one
     for world in (1, 2, 4, 8):
         got, plans, pws = emulate(engine, xyz, w, k, cfg, world)
         # every proxy weight slot at depth >= 1 has exactly one owner
@@ -69,3 +75,24 @@ def test_run_to_run_bitwise(engine, name, level):
     a = engine.csfmm_sum(p, p, k, cfg).values
     b = engine.csfmm_sum(p, p, k, cfg).values
     np.testing.assert_array_equal(a, b)
+
+
+def test_unit_scope_single_gpu_equals_partition(monkeypatch):
+    """With CSFS_B200_MUTUAL_SCOPE=unit the single-GPU csfmm pairs exactly the leaves the
+    partitioned path pairs, and the two are bitwise equal."""
+    from paper_2508_13550_b200 import Engine
+
+    monkeypatch.setenv("CSFS_B200_MUTUAL_SCOPE", "unit")
+    eng = Engine(0)
+    wl = configs.make("c5", level=6)
+    dev = torch.device("cuda", 0)
+    xyz = torch.from_numpy(wl.xyz).to(dev)
+    w = torch.from_numpy(wl.weights).to(dev)
+    k = Kernel.parse(wl.kernel)
+    cfg = TraversalConfig(mac=wl.mac, degree=wl.degree, n0=wl.n0)
+    ref_out = torch.empty(wl.n, dtype=torch.float64, device=dev)
+    eng.csfmm_device(xyz.data_ptr(), wl.n, xyz.data_ptr(), w.data_ptr(), wl.n, k, cfg, ref_out.data_ptr(),
+                     torch.cuda.current_stream().cuda_stream)
+    got, _, _ = emulate(eng, xyz, w, k, cfg, 4)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref_out.cpu().numpy())
+    eng.close()
