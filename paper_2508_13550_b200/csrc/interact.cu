@@ -211,12 +211,13 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
 // over the group's warps in fixed order: deterministic, no atomics.  Both partial sums go
 // to `partial`; k_mutual_reduce adds them to phi_near after the list items.
 struct MutualParams {
-    const int4* pair;       // {A begin, |A|, B begin, |B|}, |A|, |B| <= 256
+    const int4* pair;       // {A begin, |A|, B begin, |B|}, |A|, |B| <= 256; negative: proxy sets (CC)
     const long long* poff;  // partial offset of A's block (B's follows at + |A|)
     const int* anchor;      // A's begin, or -1: every rank
     int n_pairs;
     int* counter;  // work queue (persistent CTAs)
     const double *px, *py, *pz, *pw;  // particles (tree order) + weights
+    const double *qx, *qy, *qz, *qw;  // proxy points + proxy weights
     double* partial;
     const double2* log_tab;
     long long own_b, own_e;
@@ -243,11 +244,16 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
             if (a >= 0 && (a < P.own_b || a >= P.own_e)) continue;  // CTA-uniform
         }
         const int4 q = P.pair[p];
-        for (int j = tid; j < q.w; j += kIB) {
-            sxy[j] = make_double2(P.px[q.z + j], P.py[q.z + j]);
-            szw[j] = make_double2(P.pz[q.z + j], P.pw[q.z + j]);
+        const bool prox = q.y < 0;  // CC: both sides are proxy sets
+        const double* X = prox ? P.qx : P.px;
+        const double* Y = prox ? P.qy : P.py;
+        const double* Z = prox ? P.qz : P.pz;
+        const double* Wt = prox ? P.qw : P.pw;
+        const int tlen = prox ? -q.y : q.y, nb = prox ? -q.w : q.w;
+        for (int j = tid; j < nb; j += kIB) {
+            sxy[j] = make_double2(X[q.z + j], Y[q.z + j]);
+            szw[j] = make_double2(Z[q.z + j], Wt[q.z + j]);
         }
-        const int tlen = q.y, nb = q.w;
         const int per = (tlen + kMTPT - 1) / kMTPT;
         const int gs = min(kIB, (per + 31) & ~31);
         const int G = kIB / gs;
@@ -264,10 +270,10 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
             tz[k] = 1.0;
             tw[k] = 0.0;
             if (act[k]) {
-                tx[k] = P.px[q.x + t];
-                ty[k] = P.py[q.x + t];
-                tz[k] = P.pz[q.x + t];
-                tw[k] = P.pw[q.x + t];
+                tx[k] = X[q.x + t];
+                ty[k] = Y[q.x + t];
+                tz[k] = Z[q.x + t];
+                tw[k] = Wt[q.x + t];
             }
             acc[k] = 0.0;
         }
@@ -349,22 +355,27 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
     }
 }
 
-// phi_near[x] += every symmetric-pair partial of x's leaf, in ascending partial order.
-// One CTA per cluster; owned leaves only.
-__global__ void k_mutual_reduce(const int* __restrict__ begin, const int* __restrict__ end,
+// phi_near[x] (leaf keys X < ncl) or qphi[c*npp + m] (cluster keys X = ncl + c) += every
+// symmetric-pair partial of that point set, in ascending partial order.  One CTA per key;
+// owned sets only.
+__global__ void k_mutual_reduce(int ncl, int npp, const int* __restrict__ begin, const int* __restrict__ end,
                                 const int* __restrict__ mcnt, const int* __restrict__ moff,
                                 const long long* __restrict__ mlist, const double* __restrict__ partial,
-                                double* phi, long long own_b, long long own_e) {
+                                double* phi, double* qphi, long long own_b, long long own_e) {
     const int X = blockIdx.x;
     const int n = mcnt[X];
     if (n == 0) return;
-    const int b = begin[X], e = end[X];
+    const bool leaf = X < ncl;
+    const int c = leaf ? X : X - ncl;
+    const int b = begin[c];
     if (b < own_b || b >= own_e) return;
+    double* out = leaf ? phi + b : qphi + (long long)c * npp;
+    const int len = leaf ? end[c] - b : npp;
     const long long* l = mlist + moff[X];
-    for (int x = b + threadIdx.x; x < e; x += blockDim.x) {
-        double v = phi[x];
-        for (int a = 0; a < n; ++a) v += partial[l[a] + (x - b)];
-        phi[x] = v;
+    for (int x = threadIdx.x; x < len; x += blockDim.x) {
+        double v = out[x];
+        for (int a = 0; a < n; ++a) v += partial[l[a] + x];
+        out[x] = v;
     }
 }
 
@@ -493,6 +504,10 @@ void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src,
         m.py = src.py;
         m.pz = src.pz;
         m.pw = src.w;
+        m.qx = src.qx;
+        m.qy = src.qy;
+        m.qz = src.qz;
+        m.qw = src.qw;
         m.partial = items.partial;
         m.log_tab = log_tab;
         m.own_b = own.b;
@@ -503,8 +518,8 @@ void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src,
         launch(p, op, s);
     });
     if (items.mutual) {
-        k_mutual_reduce<<<tgt.ncl, 128, 0, s>>>(tgt.begin, tgt.end, items.mcnt, items.moff, items.mlist,
-                                                items.partial, phi_near, own.b, own.e);
+        k_mutual_reduce<<<2 * tgt.ncl, 128, 0, s>>>(tgt.ncl, tgt.npp, tgt.begin, tgt.end, items.mcnt, items.moff,
+                                                    items.mlist, items.partial, phi_near, tgt.qphi, own.b, own.e);
         CSFS_LAUNCH_CHECK();
     }
 }

@@ -125,11 +125,27 @@ __device__ __forceinline__ int unit_of(const long long* ub, int nu, long long b)
     return lo;
 }
 
-// Symmetric PP (targets == sources, scalar kernels): K(t, s) = kSym K(s, t) bit-for-bit,
-// so a PP pair of leaves {A, B} listed in BOTH directions is evaluated once by the tile
-// kernel k_mutual (both segments are dropped from the list items).  Only pairs inside one
-// partition unit (depth-1 subtree) with |A|, |B| <= 256 qualify, so the choice — and the
-// summation order — is the same for every rank count.
+// Symmetric pairs (targets == sources, scalar kernels): K(t, s) = kSym K(s, t)
+// bit-for-bit, so an interaction listed in BOTH directions is evaluated once by the tile
+// kernel k_mutual (both segments are dropped from the list items):
+//   * PP leaf pairs {A, B} (|A|, |B| <= 256): A's particles x B's particles;
+//   * CC cluster pairs {A, B}: A's (p+1)^2 proxy points x B's, weighted by the proxy
+//     weights; the partial sums land in the proxy potentials (the M2L-like far field).
+// Only targets at depth >= 1 and pairs inside one partition unit qualify (unit_b: one unit
+// = every pair), so the choice — and the summation order — is the same for every rank
+// count of the partitioned path.  Pair ids: PP = (leaf t, leaf s), CC = (ncl + t, ncl + s)
+// (the work-item keys), t < s.
+__device__ __forceinline__ bool listed(const long long* code, const int* off, const int* cnt, int key,
+                                       long long want) {
+    int lo = off[key], hi = off[key] + cnt[key];
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (code[mid] < want) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < off[key] + cnt[key] && code[lo] == want;
+}
+
 __global__ void k_mutual_mark(int n_items, int ncl_t, const int* __restrict__ keys,
                               const int* __restrict__ cnt, const int* __restrict__ off,
                               const long long* __restrict__ code, int2* seg, int* mflag, int2* epair,
@@ -141,28 +157,25 @@ __global__ void k_mutual_mark(int n_items, int ncl_t, const int* __restrict__ ke
         const int key = keys[i];
         const int b = off[key], n = cnt[key];
         for (int a = 0; a < n; ++a) mflag[b + a] = 0;
-        const int t = key;
-        const int nt = key < ncl_t ? T.end[t] - T.begin[t] : 0;
-        if (key < ncl_t && T.depth[t] >= 1 && nt <= 256) {
+        const bool leaf_item = key < ncl_t;
+        const int t = leaf_item ? key : key - ncl_t;
+        const int nt = leaf_item ? T.end[t] - T.begin[t] : T.npp;
+        if (T.depth[t] >= 1 && (!leaf_item || nt <= 256)) {
             const int ut = unit_of(unit_b, n_units, T.begin[t]);
+            const long long type = leaf_item ? 0 : 3;  // PP entries of leaf items, CC of cluster items
             for (int a = 0; a < n; ++a) {
                 const long long c = code[b + a];
-                if ((c >> 32) != 0) break;  // sorted: PP entries come first
+                if ((c >> 32) < type) continue;  // sorted by (type, source)
+                if ((c >> 32) > type) break;
                 const int s = int(c & 0xffffffffll);
-                const int ns = T.end[s] - T.begin[s];
+                const int ns = leaf_item ? T.end[s] - T.begin[s] : T.npp;
                 if (s == t || ns > 256 || T.depth[s] < 1 || unit_of(unit_b, n_units, T.begin[s]) != ut) continue;
-                int lo = off[s], hi = off[s] + cnt[s];  // is (s, t) a PP entry too?
-                const long long want = (long long)(unsigned)t;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (code[mid] < want) lo = mid + 1;
-                    else hi = mid;
-                }
-                if (lo < off[s] + cnt[s] && code[lo] == want) {
+                const int key_s = leaf_item ? s : ncl_t + s;
+                if (listed(code, off, cnt, key_s, (type << 32) | (long long)(unsigned)t)) {
                     seg[b + a].y = 0;  // both directions leave the list items
                     if (t < s) {
                         mflag[b + a] = 1;
-                        epair[b + a] = make_int2(t, s);
+                        epair[b + a] = make_int2(key, key_s);
                         sv += (unsigned long long)ns * nt;
                     }
                 }
@@ -178,7 +191,7 @@ __global__ void k_mutual_count(int n_pairs, const int4* __restrict__ pair, const
                                int* mcnt, const int2* __restrict__ pl) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n_pairs) return;
-    atomicAdd(&mcnt[pl[p].x], 1);
+    atomicAdd(&mcnt[pl[p].x], 1);  // pair ids are the work-item keys (leaf or ncl + cluster)
     atomicAdd(&mcnt[pl[p].y], 1);
 }
 
@@ -188,7 +201,7 @@ __global__ void k_mutual_fill(int n_pairs, const int4* __restrict__ pair, const 
     if (p >= n_pairs) return;
     const int A = pl[p].x, B = pl[p].y;
     mlist[moff[A] + atomicAdd(&mcur[A], 1)] = poff[p];
-    mlist[moff[B] + atomicAdd(&mcur[B], 1)] = poff[p] + pair[p].y;
+    mlist[moff[B] + atomicAdd(&mcur[B], 1)] = poff[p] + abs(pair[p].y);
 }
 
 __global__ void k_mutual_sort(int ncl, const int* __restrict__ mcnt, const int* __restrict__ moff, long long* mlist) {
@@ -234,9 +247,9 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
     const long long ne = std::max<long long>(it.n_entries, 1);
     it.mflag.grow(ne);
     it.epair.grow(ne);
-    it.mcnt.grow(ncl);
-    it.moff.grow(ncl);
-    it.mcur.grow(ncl);
+    it.mcnt.grow(2 * ncl);  // per work-item key: leaves [0, ncl), clusters' proxies [ncl, 2 ncl)
+    it.moff.grow(2 * ncl);
+    it.mcur.grow(2 * ncl);
     it.unit_b.grow(std::max<size_t>(unit_begins.size(), 1));
     it.n_mutual = 0;
     it.n_partial = 0;
@@ -245,8 +258,8 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
     CSFS_CK(cudaMemcpyAsync(it.unit_b.p, unit_begins.data(), unit_begins.size() * sizeof(long long),
                             cudaMemcpyHostToDevice, s));
     CSFS_CK(cudaMemsetAsync(it.pairs.p + 4, 0, sizeof(unsigned long long), s));
-    CSFS_CK(cudaMemsetAsync(it.mcnt.p, 0, ncl * sizeof(int), s));
-    CSFS_CK(cudaMemsetAsync(it.mcur.p, 0, ncl * sizeof(int), s));
+    CSFS_CK(cudaMemsetAsync(it.mcnt.p, 0, 2 * ncl * sizeof(int), s));
+    CSFS_CK(cudaMemsetAsync(it.mcur.p, 0, 2 * ncl * sizeof(int), s));
     const int nb = ceil_div(it.n_items, 128);
     k_mutual_mark<<<nb, 128, 0, s>>>(it.n_items, ncl, it.keys, it.cnt, it.off, it.code, it.seg, it.mflag, it.epair,
                                      it.unit_b, int(unit_begins.size()), T, it.pairs.p + 4);
@@ -260,7 +273,7 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
             if (mflag[e]) {
                 const int2 q = ep[e];
                 c[0] = 1;
-                c[1] = (T.end[q.x] - T.begin[q.x]) + (T.end[q.y] - T.begin[q.y]);
+                c[1] = q.x >= ncl ? 2 * T.npp : (T.end[q.x] - T.begin[q.x]) + (T.end[q.y] - T.begin[q.y]);
             }
         };
         auto count_only = [=] __device__(long long, const int*, const int*) {};
@@ -284,9 +297,16 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
         auto e = [=] __device__(long long i, const int* c, const int* pre) {
             if (!c[0]) return;
             const int2 q = ep[i];
-            pair[pre[0]] = make_int4(T.begin[q.x], T.end[q.x] - T.begin[q.x], T.begin[q.y], T.end[q.y] - T.begin[q.y]);
+            if (q.x >= ncl) {  // CC: proxy sets, negative lengths
+                const int a = q.x - ncl, b = q.y - ncl;
+                pair[pre[0]] = make_int4(a * T.npp, -T.npp, b * T.npp, -T.npp);
+                manchor[pre[0]] = T.begin[a];
+            } else {
+                pair[pre[0]] = make_int4(T.begin[q.x], T.end[q.x] - T.begin[q.x], T.begin[q.y],
+                                         T.end[q.y] - T.begin[q.y]);
+                manchor[pre[0]] = T.begin[q.x];
+            }
             poff[pre[0]] = pre[1];
-            manchor[pre[0]] = T.begin[q.x];
             leaf[pre[0]] = q;
         };
         if (it.n_mutual) run_scan<2>(it.n_entries, f, e, sc.tiles, sc.grand, s);
@@ -298,14 +318,14 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
     {
         const int* mcnt = it.mcnt;
         int* moff = it.moff;
-        sc.tiles.grow(scan_tile_ints(ncl, 1));
+        sc.tiles.grow(scan_tile_ints(2 * ncl, 1));
         auto f = [=] __device__(long long i, int* c) { c[0] = mcnt[i]; };
         auto e = [=] __device__(long long i, const int* c, const int* pre) { moff[i] = pre[0]; };
-        run_scan<1>(ncl, f, e, sc.tiles, sc.grand, s);
+        run_scan<1>(2 * ncl, f, e, sc.tiles, sc.grand, s);
     }
     k_mutual_fill<<<pb, 256, 0, s>>>(it.n_mutual, it.mpair, it.mpoff, it.mleaf, it.moff, it.mcur, it.mlist);
     CSFS_LAUNCH_CHECK();
-    k_mutual_sort<<<ceil_div(ncl, 128), 128, 0, s>>>(ncl, it.mcnt, it.moff, it.mlist);
+    k_mutual_sort<<<ceil_div(2 * ncl, 128), 128, 0, s>>>(2 * ncl, it.mcnt, it.moff, it.mlist);
     CSFS_LAUNCH_CHECK();
 }
 
