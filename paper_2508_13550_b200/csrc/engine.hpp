@@ -50,6 +50,13 @@ struct DevBuf {
     operator T*() const { return p; }
 };
 
+// Source segments / symmetric-pair lengths carry two flags next to the length: the sign
+// (negative = proxy points) and bit 30 of the magnitude (the coincidence guard is needed
+// for this entry; kernels_dev.cuh eval<G>).
+constexpr int kSegGuard = 1 << 30;
+__host__ __device__ __forceinline__ int seg_len(int y) { return (y < 0 ? -y : y) & (kSegGuard - 1); }
+__host__ __device__ __forceinline__ bool seg_guard(int y) { return ((y < 0 ? -y : y) & kSegGuard) != 0; }
+
 // Raw-pointer view of a tree, passed by value into kernels.
 struct TreeView {
     long long n;
@@ -63,6 +70,7 @@ struct TreeView {
     const double *xi0, *xi1, *eta0, *eta1, *cx, *cy, *cz, *rad;
     // proxies: cluster c owns [c*npp, (c+1)*npp), index k1*np+k2 (interpolation.cpp:64-67)
     const double *qx, *qy, *qz;
+    const double* qrad;  // per cluster: max chordal distance from the centre to its proxy points
 };
 
 struct DeviceTree {
@@ -84,7 +92,7 @@ struct DeviceTree {
     std::vector<int> level_first, level_count;
     std::vector<int> root_count;  // 6
     // proxies
-    DevBuf<double> qx, qy, qz;
+    DevBuf<double> qx, qy, qz, qrad;
     DevBuf<double> qw;    // proxy weights (source side), ncl*npp
     DevBuf<double> qphi;  // proxy potentials (target side), ncl*npp*dim
 

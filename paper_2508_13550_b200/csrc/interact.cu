@@ -17,6 +17,7 @@
 // This is FP64-pipe bound: the inner loop is the kernel functor.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "engine.hpp"
 #include "kernels_dev.cuh"
@@ -122,13 +123,24 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                 for (int c = 0; c < D; ++c) acc[k][c] = 0.0;
             }
             const bool any = act[0];  // slot 0 is filled first
-            auto compute = [&](int n) {
-                if (any) {
+            // guarded: the chunk holds a segment that may contain coincident pairs
+            auto compute = [&](int n, bool guarded) {
+                if (!any) return;
+                if (guarded) {
 #pragma unroll kUnroll
                     for (int j = g; j < n; j += G) {
                         const double2 a = sxy[j], b = szw[j];
 #pragma unroll
-                        for (int k = 0; k < kTPT; ++k) op(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, acc[k], tab);
+                        for (int k = 0; k < kTPT; ++k)
+                            op.template eval<true>(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, acc[k], tab);
+                    }
+                } else {
+#pragma unroll kUnroll
+                    for (int j = g; j < n; j += G) {
+                        const double2 a = sxy[j], b = szw[j];
+#pragma unroll
+                        for (int k = 0; k < kTPT; ++k)
+                            op.template eval<false>(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, acc[k], tab);
                     }
                 }
             };
@@ -138,12 +150,15 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
             static_assert(kICH == kIB, "one source slot per thread");
             int ce = d.z, cpos = 0;  // cursor into the segment list (CTA-uniform)
             double rx = 0.0, ry = 0.0, rz = 0.0, rw = 0.0;
+            bool fguard = false;  // guard flag of the chunk being fetched (CTA-uniform)
             auto fetch = [&]() {
                 int filled = 0;
+                fguard = false;
                 while (filled < kICH && ce < d.w) {
                     const int2 sg = P.seg[ce];
                     const bool sproxy = sg.y < 0;
-                    const int len = sproxy ? -sg.y : sg.y;  // 0: evaluated by the symmetric kernel
+                    const int len = seg_len(sg.y);  // 0: evaluated by the symmetric kernel
+                    fguard = fguard || (len > 0 && seg_guard(sg.y));
                     const int take = min(len - cpos, kICH - filled);
                     if (tid >= filled && tid < filled + take) {
                         const long long src = (long long)sg.x + cpos + (tid - filled);
@@ -162,6 +177,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                 return filled;
             };
             int n = fetch();
+            bool guarded = fguard;
             while (n > 0) {
                 if (tid < n) {
                     sxy[tid] = make_double2(rx, ry);
@@ -169,9 +185,13 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                 }
                 __syncthreads();
                 const int next = fetch();  // loads in flight during compute
-                compute(n);
+#ifdef CSFS_FORCE_GUARD
+                guarded = CSFS_FORCE_GUARD;
+#endif
+                compute(n, guarded);
                 __syncthreads();
                 n = next;
+                guarded = fguard;
             }
             if (G > 1) {
 #pragma unroll
@@ -245,11 +265,16 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
         }
         const int4 q = P.pair[p];
         const bool prox = q.y < 0;  // CC: both sides are proxy sets
+#ifdef CSFS_FORCE_GUARD
+        const bool guarded = CSFS_FORCE_GUARD;
+#else
+        const bool guarded = seg_guard(q.y);
+#endif
         const double* X = prox ? P.qx : P.px;
         const double* Y = prox ? P.qy : P.py;
         const double* Z = prox ? P.qz : P.pz;
         const double* Wt = prox ? P.qw : P.pw;
-        const int tlen = prox ? -q.y : q.y, nb = prox ? -q.w : q.w;
+        const int tlen = seg_len(q.y), nb = seg_len(q.w);
         for (int j = tid; j < nb; j += kIB) {
             sxy[j] = make_double2(X[q.z + j], Y[q.z + j]);
             szw[j] = make_double2(Z[q.z + j], Wt[q.z + j]);
@@ -283,17 +308,18 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
             // over the warp by a transposed butterfly: 4+2+1+1+1 shuffles for 8 sources
             constexpr int kB = 8;
             const int full_end = nb - (kB - 1) * G;  // j < full_end: all 8 sources exist
-            auto sources = [&](int j, double (&c)[kB], bool guard) {
+            // tail: the last batch may be short; kG: the coincidence guard (pair-uniform)
+            auto sources = [&](int j, double (&c)[kB], bool tail, auto kG) {
 #pragma unroll
                 for (int m = 0; m < kB; ++m) {
                     c[m] = 0.0;
                     const int jm = j + m * G;
-                    if (!guard || jm < nb) {  // group-uniform
+                    if (!tail || jm < nb) {  // group-uniform
                         const double2 a = sxy[jm], b = szw[jm];
 #pragma unroll
                         for (int k = 0; k < kMTPT; ++k) {
                             double K[1];
-                            op.value(tx[k], ty[k], tz[k], a.x, a.y, b.x, K, tab);
+                            op.template value<decltype(kG)::value>(tx[k], ty[k], tz[k], a.x, a.y, b.x, K, tab);
                             acc[k] = fma(b.y, K[0], acc[k]);
                             c[m] = fma(tw[k], K[0], c[m]);
                         }
@@ -302,8 +328,13 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
             };
             for (int j = g; j < nb; j += kB * G) {
                 double c[kB];
-                if (j < full_end) sources(j, c, false);
-                else sources(j, c, true);
+                if (guarded) {
+                    if (j < full_end) sources(j, c, false, std::true_type{});
+                    else sources(j, c, true, std::true_type{});
+                } else {
+                    if (j < full_end) sources(j, c, false, std::false_type{});
+                    else sources(j, c, true, std::false_type{});
+                }
                 const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
                 double v4[4], v2[2];
 #pragma unroll
@@ -543,8 +574,9 @@ void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, cons
         CSFS_LAUNCH_CHECK();
     }
     std::vector<int2> hseg;
-    const long long kSeg = 1 << 30;
-    for (long long b = 0; b < ns; b += kSeg) hseg.push_back(make_int2(int(b), int(std::min(kSeg, ns - b))));
+    const long long kSeg = 1 << 29;  // below the guard flag bit
+    for (long long b = 0; b < ns; b += kSeg)
+        hseg.push_back(make_int2(int(b), int(std::min(kSeg, ns - b)) | kSegGuard));
     const int nseg = int(hseg.size());
     segs.grow(std::max(nseg, 1));
     if (nseg) CSFS_CK(cudaMemcpyAsync(segs.p, hseg.data(), nseg * sizeof(int2), cudaMemcpyHostToDevice, s));

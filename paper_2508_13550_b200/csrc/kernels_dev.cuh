@@ -24,25 +24,33 @@ namespace csfs_b200 {
 // Each op also provides value(): the unscaled, guarded K(t, s) (0 where the guard skips),
 // used by the symmetric PP path, which applies one evaluation to both the target's row
 // and the source's column; kSym: K(s, t) = kSym * K(t, s) (exactly: the unfused dot and
-// cross products commute bit-for-bit).
+// cross products commute bit-for-bit).  eval<G> / value<G>: G = false drops the
+// coincidence guard, for list entries proven free of pairs with 1 - x.y < 1e-14
+// (needs_guard, traverse.cu) — the same values with 5 fewer issue slots per pair.
 struct OpLaplace {
     static constexpr int dim = 1;
     static constexpr double kSym = 1.0;
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
+    template <bool G = true>
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = not_coincident(omc);
-        const double v = fast_log(safe_omc(ok, omc), tab);
+        const bool ok = !G || not_coincident(omc);
+        const double v = fast_log(G ? safe_omc(ok, omc) : omc, tab);
         K[0] = ok ? v : 0.0;
+    }
+    template <bool G = true>
+    __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
+                                         double* acc, const LogTable& tab) const {
+        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = !G || not_coincident(omc);
+        const double v = fast_log(G ? safe_omc(ok, omc) : omc, tab);
+        acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
     }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,
                                                const LogTable& tab) const {
-        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = not_coincident(omc);
-        const double v = fast_log(safe_omc(ok, omc), tab);
-        acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
+        eval<true>(tx, ty, tz, sx, sy, sz, sw, acc, tab);
     }
 };
 
@@ -88,19 +96,25 @@ struct OpBiharmonic {
     static constexpr int dim = 1;
     static constexpr double kSym = 1.0;
     __device__ __forceinline__ double scale() const { return kInv4Pi; }
+    template <bool G = true>  // regular at coincidence: no guard either way
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
         const double d = dot_ref(tx, ty, tz, sx, sy, sz);
         const double u0 = __dmul_rn(0.5, __dadd_rn(1.0, d));
         K[0] = dilog_dev((u0 < 1.0) ? u0 : 1.0, tab);
     }
-    __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
-                                               double sz, double sw, double* acc,
-                                               const LogTable& tab) const {
+    template <bool G = true>
+    __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
+                                         double* acc, const LogTable& tab) const {
         const double d = dot_ref(tx, ty, tz, sx, sy, sz);
         const double u0 = __dmul_rn(0.5, __dadd_rn(1.0, d));
         const double u = (u0 < 1.0) ? u0 : 1.0;  // std::min(1.0, u0)
         acc[0] = fma(sw, dilog_dev(u, tab), acc[0]);
+    }
+    __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
+                                               double sz, double sw, double* acc,
+                                               const LogTable& tab) const {
+        eval<true>(tx, ty, tz, sx, sy, sz, sw, acc, tab);
     }
 };
 
@@ -108,21 +122,22 @@ struct OpBiotSavart {
     static constexpr int dim = 3;
     static constexpr double kSym = -1.0;  // cross(s, t) = -cross(t, s), 1 - s.t = 1 - t.s
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
+    template <bool G = true>
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable&) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = not_coincident(omc);
-        const double a = ok ? fast_rcp(safe_omc(ok, omc)) : 0.0;
+        const bool ok = !G || not_coincident(omc);
+        const double a = ok ? fast_rcp(G ? safe_omc(ok, omc) : omc) : 0.0;
         K[0] = a * __dsub_rn(__dmul_rn(ty, sz), __dmul_rn(tz, sy));
         K[1] = a * __dsub_rn(__dmul_rn(tz, sx), __dmul_rn(tx, sz));
         K[2] = a * __dsub_rn(__dmul_rn(tx, sy), __dmul_rn(ty, sx));
     }
-    __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
-                                               double sz, double sw, double* acc,
-                                               const LogTable&) const {
+    template <bool G = true>
+    __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
+                                         double* acc, const LogTable&) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = not_coincident(omc);
-        const double a = (ok ? sw : 0.0) * fast_rcp(safe_omc(ok, omc));
+        const bool ok = !G || not_coincident(omc);
+        const double a = (ok ? sw : 0.0) * fast_rcp(G ? safe_omc(ok, omc) : omc);
         // cross(x, y) unfused, in the reference's order (geometry.hpp:20-22): for close
         // pairs the components cancel, and a contracted form would differ from it
         const double cx = __dsub_rn(__dmul_rn(ty, sz), __dmul_rn(tz, sy));
@@ -131,6 +146,10 @@ struct OpBiotSavart {
         acc[0] = fma(a, cx, acc[0]);
         acc[1] = fma(a, cy, acc[1]);
         acc[2] = fma(a, cz, acc[2]);
+    }
+    __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
+                                               double sz, double sw, double* acc, const LogTable& tab) const {
+        eval<true>(tx, ty, tz, sx, sy, sz, sw, acc, tab);
     }
 };
 
@@ -161,20 +180,26 @@ struct OpSalT {
         const double L = fast_log(fma(s, s, s), tab);
         return kLogOnly ? L : fma(k, L, r);
     }
+    template <bool G = true>
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
         const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = not_coincident(omc);
-        const double v = kernel(safe_omc(ok, omc), tab);
+        const bool ok = !G || not_coincident(omc);
+        const double v = kernel(G ? safe_omc(ok, omc) : omc, tab);
         K[0] = ok ? v : 0.0;
+    }
+    template <bool G = true>
+    __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
+                                         double* acc, const LogTable& tab) const {
+        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = !G || not_coincident(omc);
+        const double v = kernel(G ? safe_omc(ok, omc) : omc, tab);
+        acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
     }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,
                                                const LogTable& tab) const {
-        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = not_coincident(omc);
-        const double v = kernel(safe_omc(ok, omc), tab);
-        acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
+        eval<true>(tx, ty, tz, sx, sy, sz, sw, acc, tab);
     }
 };
 using OpSal = OpSalT<false>;

@@ -48,6 +48,29 @@ __device__ __forceinline__ int classify(const TreeView& T, const TreeView& S, in
     return 0;
 }
 
+// Can a list entry contain a pair with 1 - x.y < 1e-14 (the kernels' coincidence guard)?
+// t / s: target / source cluster; *_prox: that side is the cluster's proxy points (else
+// its particles).  Proven free (false) when the two point sets are separated by more than
+// 1e-6 (chordal; the guard triggers below ~1.4e-7), either by the bounding spheres
+// (centre distance minus particle / proxy radii) or, for particle sets on one cube face,
+// by a gap of more than 1e-4 rad between their shrunk (xi, eta) boxes (the equiangular map
+// shrinks distances by at most a small constant factor).  Same cluster of the same tree:
+// always guarded.
+__device__ __forceinline__ bool needs_guard(const TreeView& T, const TreeView& S, int t, bool t_prox, int s,
+                                            bool s_prox) {
+    if (T.px == S.px && t == s && !t_prox && !s_prox) return true;
+    const double dx = T.cx[t] - S.cx[s], dy = T.cy[t] - S.cy[s], dz = T.cz[t] - S.cz[s];
+    const double R = sqrt(dx * dx + dy * dy + dz * dz);
+    const double rt = t_prox ? T.qrad[t] : T.rad[t], rs = s_prox ? S.qrad[s] : S.rad[s];
+    if (R - rt - rs > 1e-6) return false;
+    if (!t_prox && !s_prox && T.face[t] == S.face[s]) {
+        const double gx = fmax(S.xi0[s] - T.xi1[t], T.xi0[t] - S.xi1[s]);
+        const double ge = fmax(S.eta0[s] - T.eta1[t], T.eta0[t] - S.eta1[s]);
+        if (fmax(gx, ge) > 1e-4) return false;
+    }
+    return true;
+}
+
 __global__ void k_count(const int2* __restrict__ l, long long n, int key_off, int* cnt,
                         const TreeView T, const TreeView S, int type, unsigned long long* pairs) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -96,18 +119,21 @@ __global__ void k_items(int n_items, int ncl_t, const int* __restrict__ keys,
         c[j + 1] = v;
     }
     long long src_pts = 0;
+    const int t = key < ncl_t ? key : key - ncl_t;
+    const bool t_prox = key >= ncl_t;
     for (int a = 0; a < n; ++a) {
         const int type = int(c[a] >> 32);
         const int s = int(c[a] & 0xffffffffll);
-        if (type == 0 || type == 2) {
-            seg[b + a] = make_int2(S.begin[s], S.end[s] - S.begin[s]);
+        const bool s_prox = !(type == 0 || type == 2);
+        const int g = needs_guard(T, S, t, t_prox, s, s_prox) ? kSegGuard : 0;
+        if (!s_prox) {
+            seg[b + a] = make_int2(S.begin[s], (S.end[s] - S.begin[s]) | g);
             src_pts += S.end[s] - S.begin[s];
         } else {
-            seg[b + a] = make_int2(s * S.npp, -S.npp);
+            seg[b + a] = make_int2(s * S.npp, -(S.npp | g));
             src_pts += S.npp;
         }
     }
-    const int t = key < ncl_t ? key : key - ncl_t;
     const int tl = key < ncl_t ? T.end[t] - T.begin[t] : T.npp;
     if (key < ncl_t) item[i] = make_int4(T.begin[t], tl, b, b + n);
     else item[i] = make_int4(t * T.npp, -T.npp, b, b + n);
@@ -201,7 +227,7 @@ __global__ void k_mutual_fill(int n_pairs, const int4* __restrict__ pair, const 
     if (p >= n_pairs) return;
     const int A = pl[p].x, B = pl[p].y;
     mlist[moff[A] + atomicAdd(&mcur[A], 1)] = poff[p];
-    mlist[moff[B] + atomicAdd(&mcur[B], 1)] = poff[p] + abs(pair[p].y);
+    mlist[moff[B] + atomicAdd(&mcur[B], 1)] = poff[p] + seg_len(pair[p].y);
 }
 
 __global__ void k_mutual_sort(int ncl, const int* __restrict__ mcnt, const int* __restrict__ moff, long long* mlist) {
@@ -299,10 +325,12 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
             const int2 q = ep[i];
             if (q.x >= ncl) {  // CC: proxy sets, negative lengths
                 const int a = q.x - ncl, b = q.y - ncl;
-                pair[pre[0]] = make_int4(a * T.npp, -T.npp, b * T.npp, -T.npp);
+                const int g = needs_guard(T, T, a, true, b, true) ? kSegGuard : 0;
+                pair[pre[0]] = make_int4(a * T.npp, -(T.npp | g), b * T.npp, -T.npp);
                 manchor[pre[0]] = T.begin[a];
             } else {
-                pair[pre[0]] = make_int4(T.begin[q.x], T.end[q.x] - T.begin[q.x], T.begin[q.y],
+                const int g = needs_guard(T, T, q.x, false, q.y, false) ? kSegGuard : 0;
+                pair[pre[0]] = make_int4(T.begin[q.x], (T.end[q.x] - T.begin[q.x]) | g, T.begin[q.y],
                                          T.end[q.y] - T.begin[q.y]);
                 manchor[pre[0]] = T.begin[q.x];
             }

@@ -377,6 +377,23 @@ __global__ void k_proxy(int ncl, int np, Cheb cheb, const int* __restrict__ face
     qz[g] = z;
 }
 
+// Proxy radius: the farthest proxy point from the cluster centre (chordal).  The
+// evaluation kernels use it, with the particle radius, to prove a list entry free of
+// coincident pairs (kernels_dev.cuh needs_guard).
+__global__ void k_qrad(int ncl, int npp, const double* __restrict__ cx, const double* __restrict__ cy,
+                       const double* __restrict__ cz, const double* __restrict__ qx, const double* __restrict__ qy,
+                       const double* __restrict__ qz, double* qrad) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncl) return;
+    double r2 = 0.0;
+    for (int k = 0; k < npp; ++k) {
+        const long long g = (long long)c * npp + k;
+        const double dx = qx[g] - cx[c], dy = qy[g] - cy[c], dz = qz[g] - cz[c];
+        r2 = fmax(r2, dx * dx + dy * dy + dz * dz);
+    }
+    qrad[c] = sqrt(r2);
+}
+
 __global__ void k_gather(long long n, const int* __restrict__ perm, const double* __restrict__ src,
                          double* __restrict__ dst) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -470,6 +487,7 @@ TreeView DeviceTree::view() const {
     v.cz = cz;
     v.rad = rad;
     v.qx = qx;
+    v.qrad = qrad;
     v.qy = qy;
     v.qz = qz;
     return v;
@@ -634,6 +652,9 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
     t.qz.grow(nq);
     k_proxy<<<ceil_div(nq, kThreads), kThreads, 0, s>>>(t.ncl, t.np, cheb, t.face, t.xi0, t.xi1,
                                                           t.eta0, t.eta1, t.qx, t.qy, t.qz);
+    CSFS_LAUNCH_CHECK();
+    t.qrad.grow(std::max(t.ncl, 1));
+    k_qrad<<<ceil_div(t.ncl, kThreads), kThreads, 0, s>>>(t.ncl, t.npp, t.cx, t.cy, t.cz, t.qx, t.qy, t.qz, t.qrad);
     CSFS_LAUNCH_CHECK();
 }
 
