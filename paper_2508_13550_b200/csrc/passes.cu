@@ -5,9 +5,10 @@
 // These are HBM/latency-bound tensor-product barycentric contractions over (p+1)^2
 // Chebyshev-2 proxy grids (K7, K8, K12, K13 in SURVEY.md §2.3).  One CTA per cluster;
 // the per-particle 1-D bases live in shared memory, every output coefficient is owned by
-// exactly one thread (deterministic, no atomics).  The leaf P2M keeps the reference's
-// accumulation order (particles ascending, a = w*Lx[k1], += a*Ly[k2]) with unfused
-// arithmetic; L2L is done separably (roundoff-level difference).
+// exactly one thread (deterministic, no atomics).  The leaf P2M forms a = w*Lx[k1] like
+// the reference and accumulates a*Ly[k2] with FMAs into four interleaved partial sums per
+// coefficient (fixed order; roundoff-level difference from the reference's serial sum,
+// within the 1e-12 proxy-weight bar); L2L is done separably.
 #include <algorithm>
 
 #include "engine.hpp"
@@ -18,7 +19,7 @@ namespace csfs_b200 {
 namespace {
 
 constexpr int kPassThreads = 128;
-constexpr int kP2mChunk = 64;
+constexpr int kP2mChunk = kPassThreads;  // particles per P2M chunk: one per thread
 
 // Leaf P2M (cluster_tree.cpp:180-191).  Internal clusters are written by k_m2m.
 // Which clusters a pass touches: mode 0 all, 1 owned at depth >= 1, 2 depth 0 only.
@@ -28,45 +29,62 @@ __device__ __forceinline__ bool selected(const TreeView& t, int c, int mode, Own
     return t.depth[c] >= 1 && t.begin[c] >= own.b && t.begin[c] < own.e;
 }
 
+template <int NP>
 __global__ void __launch_bounds__(kPassThreads)
     k_p2m(TreeView t, Cheb cheb, const double* __restrict__ w, double* __restrict__ qw, int mode,
           Own own) {
     extern __shared__ double sm[];
     const int c = blockIdx.x;
     if (t.nchild[c] > 0 || !selected(t, c, mode, own)) return;
-    const int np = cheb.np, npp = np * np;
+    const int np = NP > 0 ? NP : cheb.np, npp = np * np;
     double* WL = sm;                    // kP2mChunk x np   (w * Lx)
     double* LY = sm + kP2mChunk * np;   // kP2mChunk x np
     const int b = t.begin[c], e = t.end[c];
     const double x0 = t.xi0[c], x1 = t.xi1[c], e0 = t.eta0[c], e1 = t.eta1[c];
     const double xm = __dmul_rn(0.5, __dadd_rn(x0, x1)), xh = __dmul_rn(0.5, __dsub_rn(x1, x0));
     const double em = __dmul_rn(0.5, __dadd_rn(e0, e1)), eh = __dmul_rn(0.5, __dsub_rn(e1, e0));
-    double acc[(kMaxNp * kMaxNp + kPassThreads - 1) / kPassThreads];
+    constexpr int M = NP > 0 ? NP : kMaxNp;
+    constexpr int kOut = (M * M + kPassThreads - 1) / kPassThreads;  // outputs per thread
+    double acc[kOut][4];  // 4 interleaved partial sums per output (ILP on the add chain)
 #pragma unroll
-    for (int i = 0; i < (kMaxNp * kMaxNp + kPassThreads - 1) / kPassThreads; ++i) acc[i] = 0.0;
+    for (int q = 0; q < kOut; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[q][r] = 0.0;
     for (int base = b; base < e; base += kP2mChunk) {
         const int m = min(kP2mChunk, e - base);
-        if (threadIdx.x < m) {
-            const int p = base + threadIdx.x;
-            double* wl = WL + threadIdx.x * np;
-            double* ly = LY + threadIdx.x * np;
-            bary1d_fast(cheb, ref_coord(t.xi[p], xm, xh), wl);
-            bary1d_fast(cheb, ref_coord(t.eta[p], em, eh), ly);
-            const double wt = w[p];
-            for (int k = 0; k < np; ++k) wl[k] = __dmul_rn(wt, wl[k]);
+        for (int j = threadIdx.x; j < m; j += kPassThreads) {  // one particle per thread
+            double lx[M], ly[M];
+            bary1d_fast<NP>(cheb, ref_coord(t.xi[base + j], xm, xh), lx);
+            bary1d_fast<NP>(cheb, ref_coord(t.eta[base + j], em, eh), ly);
+            const double wt = w[base + j];
+#pragma unroll
+            for (int k = 0; k < M; ++k)
+                if (k < np) {
+                    WL[j * np + k] = __dmul_rn(wt, lx[k]);
+                    LY[j * np + k] = ly[k];
+                }
         }
         __syncthreads();
-        int idx = 0;
-        for (int o = threadIdx.x; o < npp; o += kPassThreads, ++idx) {
-            const int k1 = o / np, k2 = o % np;
-            double a = acc[idx];
-            for (int j = 0; j < m; ++j) a = __dadd_rn(a, __dmul_rn(WL[j * np + k1], LY[j * np + k2]));
-            acc[idx] = a;
+#pragma unroll
+        for (int q = 0; q < kOut; ++q) {
+            const int o = threadIdx.x + q * kPassThreads;
+            if (o < npp) {
+                const int k1 = o / np, k2 = o % np;
+                int j = 0;
+                for (; j + 4 <= m; j += 4)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        acc[q][r] = fma(WL[(j + r) * np + k1], LY[(j + r) * np + k2], acc[q][r]);
+                for (; j < m; ++j) acc[q][j & 3] = fma(WL[j * np + k1], LY[j * np + k2], acc[q][j & 3]);
+            }
         }
         __syncthreads();
     }
-    int idx = 0;
-    for (int o = threadIdx.x; o < npp; o += kPassThreads, ++idx) qw[(long long)c * npp + o] = acc[idx];
+#pragma unroll
+    for (int q = 0; q < kOut; ++q) {
+        const int o = threadIdx.x + q * kPassThreads;
+        if (o < npp) qw[(long long)c * npp + o] = (acc[q][0] + acc[q][1]) + (acc[q][2] + acc[q][3]);
+    }
 }
 
 // Transfer matrix columns: At[m*np + k] = L^parent_k(child node m)  (transfer_matrix, :16-25).
@@ -239,7 +257,13 @@ void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s, int mode, Ow
     }
     const size_t sm_p2m = size_t(2) * kP2mChunk * np * sizeof(double);
     const int n_p2m = mode == 2 ? src.level_count[0] : src.ncl;  // depth 0 = ids 0..5
-    k_p2m<<<n_p2m, kPassThreads, sm_p2m, s>>>(v, cheb, src.w, src.qw, mode, own);
+    auto p2m = [&](auto kern) { kern<<<n_p2m, kPassThreads, sm_p2m, s>>>(v, cheb, src.w, src.qw, mode, own); };
+    switch (np) {
+        case 7: p2m(k_p2m<7>); break;
+        case 9: p2m(k_p2m<9>); break;
+        case 11: p2m(k_p2m<11>); break;
+        default: p2m(k_p2m<0>);
+    }
     CSFS_LAUNCH_CHECK();
     const size_t sm_m2m = size_t(3) * npp * sizeof(double);
     const int lo = mode == 1 ? 1 : 0;
