@@ -189,8 +189,11 @@ __global__ void __launch_bounds__(kPassThreads)
 // L2P (cluster_tree.cpp:241-255) fused with the final scatter to input order:
 // out[perm[t]] = near[t] + sum_k Lx[k1] Ly[k2] P[k].  NP > 0: compile-time (p+1), bases in
 // registers; NP = 0: any degree.
+#ifndef CSFS_L2P_MINB
+#define CSFS_L2P_MINB 8
+#endif
 template <int NP, int D>
-__global__ void __launch_bounds__(kPassThreads)
+__global__ void __launch_bounds__(kPassThreads, CSFS_L2P_MINB)
     k_l2p(TreeView t, Cheb cheb, const double* __restrict__ qphi, const double* __restrict__ near,
           double* __restrict__ out, Own own, bool out_perm) {
     extern __shared__ double sm[];
@@ -212,18 +215,23 @@ __global__ void __launch_bounds__(kPassThreads)
         double f[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) f[d] = 0.0;
+        // separably: f = sum_k1 Lx[k1] (sum_k2 Ly[k2] P[k1][k2])  (np^2 + np FMAs per output
+        // component instead of 2 np^2; roundoff-level difference from the reference's order)
 #pragma unroll
         for (int k1 = 0; k1 < M; ++k1) {
             if (k1 >= np) break;
-            const double a = lx[k1];
             const double* row = sm + k1 * np * D;
+            double g[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) g[d] = 0.0;
 #pragma unroll
             for (int k2 = 0; k2 < M; ++k2) {
                 if (k2 >= np) break;
-                const double bb = a * ly[k2];
 #pragma unroll
-                for (int d = 0; d < D; ++d) f[d] = fma(bb, row[k2 * D + d], f[d]);
+                for (int d = 0; d < D; ++d) g[d] = fma(ly[k2], row[k2 * D + d], g[d]);
             }
+#pragma unroll
+            for (int d = 0; d < D; ++d) f[d] = fma(lx[k1], g[d], f[d]);
         }
         const long long dst = (long long)(out_perm ? t.perm[p] : p) * D;
 #pragma unroll
