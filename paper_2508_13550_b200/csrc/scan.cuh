@@ -18,9 +18,9 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-template <int K>
+template <int K, int THREADS = kScanThreads>
 __device__ __forceinline__ void block_exclusive_scan(int (&v)[K], int (&total)[K]) {
-    __shared__ int warp_tot[kScanThreads / 32][K];
+    __shared__ int warp_tot[THREADS / 32][K];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int incl[K];
 #pragma unroll
@@ -40,7 +40,7 @@ __device__ __forceinline__ void block_exclusive_scan(int (&v)[K], int (&total)[K
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         int pre = 0, tot = 0;
-        for (int w = 0; w < kScanThreads / 32; ++w) {
+        for (int w = 0; w < THREADS / 32; ++w) {
             const int t = warp_tot[w][k];
             if (w < warp) pre += t;
             tot += t;
@@ -78,21 +78,37 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_totals(long long n, F 
 }
 
 // One CTA: exclusive scan of the tile totals (in place -> offsets), grand totals out.
+// 256 threads x 4 consecutive tiles per pass: a C5 level (6,144 tiles) takes 6 passes.
+constexpr int kTileScanThreads = 256;
+constexpr int kTileScanItems = 4;
+
 template <int K>
-__global__ void __launch_bounds__(kScanThreads) scan_tiles(int ntiles, int* tile_tot, int* grand) {
+__global__ void __launch_bounds__(kTileScanThreads) scan_tiles(int ntiles, int* tile_tot, int* grand) {
     int carry[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) carry[k] = 0;
-    for (int b0 = 0; b0 < ntiles; b0 += kScanThreads) {
-        const int b = b0 + threadIdx.x;
-        int v[K];
+    constexpr int kPass = kTileScanThreads * kTileScanItems;
+    for (int b0 = 0; b0 < ntiles; b0 += kPass) {
+        const int b = b0 + threadIdx.x * kTileScanItems;
+        int v[kTileScanItems][K], t[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) v[k] = b < ntiles ? tile_tot[(long long)b * K + k] : 0;
+        for (int k = 0; k < K; ++k) t[k] = 0;
+#pragma unroll
+        for (int j = 0; j < kTileScanItems; ++j)
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                v[j][k] = (b + j < ntiles) ? tile_tot[(long long)(b + j) * K + k] : 0;
+                t[k] += v[j][k];
+            }
         int tot[K];
-        block_exclusive_scan<K>(v, tot);
-        if (b < ntiles)
+        block_exclusive_scan<K, kTileScanThreads>(t, tot);
 #pragma unroll
-            for (int k = 0; k < K; ++k) tile_tot[(long long)b * K + k] = v[k] + carry[k];
+        for (int j = 0; j < kTileScanItems; ++j)
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (b + j < ntiles) tile_tot[(long long)(b + j) * K + k] = t[k] + carry[k];
+                t[k] += v[j][k];
+            }
 #pragma unroll
         for (int k = 0; k < K; ++k) carry[k] += tot[k];
     }
@@ -145,7 +161,7 @@ void run_scan(long long n, F f, E e, int* tile_buf, int* grand, cudaStream_t str
     const int ntiles = ceil_div(n, kScanTile);
     scan_tile_totals<K><<<ntiles, kScanThreads, 0, stream>>>(n, f, tile_buf);
     CSFS_LAUNCH_CHECK();
-    scan_tiles<K><<<1, kScanThreads, 0, stream>>>(ntiles, tile_buf, grand);
+    scan_tiles<K><<<1, kTileScanThreads, 0, stream>>>(ntiles, tile_buf, grand);
     CSFS_LAUNCH_CHECK();
     scan_emit<K><<<ntiles, kScanThreads, 0, stream>>>(n, f, tile_buf, e);
     CSFS_LAUNCH_CHECK();
