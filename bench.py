@@ -263,7 +263,7 @@ def main():
                                  "biot_savart": "bs"}[wl.kernel])
         traffic = ncu.get("dram_bytes_per_launch")
         exec_fpp = ncu.get("fp64_flop_per_pair_executed")
-        exec_evals = s0.evals_executed  # symmetric PP pairs evaluated once for both directions
+        exec_evals = s0.evals_executed  # symmetric PP/CC pairs evaluated once for both directions
         roof = {"bound": "fp64", "kernel": f"evaluation phase: k_mutual + k_interact<Op{wl.kernel}> "
                                           f"(PP+PC+CP+CC)", "achieved": achieved,
                 "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,

@@ -66,8 +66,8 @@ typedef struct {
     double t_lists, t_interact;                  /* sub-phases of t_traversal */
     uint64_t evals_pp, evals_pc, evals_cp, evals_cc; /* pairwise kernel evaluations */
     int shared_tree;                             /* targets == sources: one tree built */
-    uint64_t evals_executed;  /* kernel evaluations actually performed (symmetric PP pairs once) */
-    int symmetric_pairs;      /* PP leaf pairs evaluated once for both directions */
+    uint64_t evals_executed;  /* kernel evaluations actually performed (symmetric PP/CC pairs once) */
+    int symmetric_pairs;      /* PP leaf / CC cluster pairs evaluated once for both directions */
 } csfs_b200_stats;
 
 /* --- lifetime ------------------------------------------------------------------------ */

@@ -43,7 +43,7 @@ struct csfs_b200_ctx {
     bool have_state = false;
     bool have_src_tree = false;  // the last call was cstc: only the source tree exists
     int dim = 1;
-    bool use_mutual = true;  // symmetric PP evaluation (CSFS_B200_NO_SYMMETRIC=1 disables)
+    bool use_mutual = true;  // symmetric PP/CC evaluation (CSFS_B200_NO_SYMMETRIC=1 disables)
     bool mutual_unit_scope = false;  // CSFS_B200_MUTUAL_SCOPE=unit: single-GPU pairs like the partitioned path
     // multi-GPU partition state (csfs_b200_part_*)
     bool part_planned = false;

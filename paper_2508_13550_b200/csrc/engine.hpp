@@ -134,7 +134,7 @@ struct Items {
     int n_items = 0;
     long long n_entries = 0;
     unsigned long long pair_evals[4] = {0, 0, 0, 0};
-    // symmetric PP (build_mutual): per entry flag/leaf pair; per symmetric pair its
+    // symmetric PP/CC pairs (build_mutual): per entry flag/pair keys; per symmetric pair its
     // {A begin, |A|, B begin, |B|}, partial offset (A block, then B block), owner anchor;
     // per leaf the partial blocks k_mutual_reduce adds to it (sorted)
     DevBuf<int> mflag, manchor, mcnt, moff, mcur;

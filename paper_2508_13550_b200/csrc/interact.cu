@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
     }
 }
 
-// ---- symmetric PP (scalar kernels, targets == sources) ------------------------------------
+// ---- symmetric PP / CC pairs (scalar kernels, targets == sources) --------------------------
 // One CTA per leaf pair {A, B} listed in BOTH directions (A < B): every K(a, b) is
 // evaluated ONCE and applied to both sides — row sums to A, column sums to B
 // (K(b, a) = kSym K(a, b) bit-for-bit).  Same register/shared-memory structure as

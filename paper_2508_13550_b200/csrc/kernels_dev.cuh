@@ -22,7 +22,7 @@
 namespace csfs_b200 {
 
 // Each op also provides value(): the unscaled, guarded K(t, s) (0 where the guard skips),
-// used by the symmetric PP path, which applies one evaluation to both the target's row
+// used by the symmetric PP/CC path, which applies one evaluation to both the target's row
 // and the source's column; kSym: K(s, t) = kSym * K(t, s) (exactly: the unfused dot and
 // cross products commute bit-for-bit).  eval<G> / value<G>: G = false drops the
 // coincidence guard, for list entries proven free of pairs with 1 - x.y < 1e-14
