@@ -27,8 +27,7 @@ __global__ void __launch_bounds__(kCstcThreads)
            const double* __restrict__ sw, const double* __restrict__ qw, double mac, int n0, Op op,
            const double2* __restrict__ log_tab, double* __restrict__ out, unsigned long long* counts) {
     constexpr int D = Op::dim;
-    __shared__ LogTableSmem tab_sm;
-    const LogTable tab = stage_log_table(tab_sm, log_tab);
+    const LogTable tab{log_tab};  // read through L1 (many small CTAs: no per-CTA staging)
     __syncthreads();
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long npp_ = 0, npc = 0;

@@ -4,15 +4,14 @@
 // ~28 FP64 instructions, sqrt and a/b ~8 each; the kernel functors need:
 //   log   -> Tang-style table method with an accurate table (Gal): x = 2^k m with
 //            m in [0.7070, 1.4141) (so both sides of x = 1 have k = 0), m r_i = 1 + t,
-//            |t| <= 2^-9, from a 512-entry shared-memory table of {r_i, L_i}: r_i is chosen
-//            near 1/centre_i so that L_i = -ln r_i is within 2^-67 of the 2^-46 grid
-//            (tools/gen_log_table.c), hence k ln2_hi + L_i is exact in one FMA and no
-//            low-order table word is needed: one conflict-prone LDS.128 per lookup, no
-//            register-pair assembly.  The two intervals around 1 use r = 1, L = 0, so
-//            t = m - 1 is exact and log keeps full relative accuracy where log(x) ~ 0 —
-//            branch-free.  log1p(t) by a degree-6 polynomial.  10 FP64 instructions (+ one
-//            int->double conversion on the XU pipe), <= 1 ulp (mpmath check in
-//            tests/test_gpu_numerics.py).  Domain: positive normals.
+//            |t| <= 2^-11, from a 2048-entry table of {r_i, L_i} (32 KB, dynamic shared
+//            memory): r_i is chosen near 1/centre_i so that L_i = -ln r_i is within 2^-67
+//            of the 2^-46 grid (tools/gen_log_table.c), hence k ln2_hi + L_i is exact in
+//            one FMA and no low-order table word is needed: one LDS.128 per lookup.  The two
+//            intervals around 1 use r = 1, L = 0, so t = m - 1 is exact and log keeps full
+//            relative accuracy where log(x) ~ 0 — branch-free.  log1p(t) by a degree-5
+//            polynomial.  9 FP64 instructions (+ one int->double conversion on the XU pipe),
+//            <= 1 ulp (mpmath check in tests/test_gpu_numerics.py).  Domain: positive normals.
 //   rsqrt -> MUFU.RSQ64H seed + one cubic-convergent correction (5 FP64), <= 2 ulp.
 //   rcp   -> MUFU.RCP64H seed + one cubic-convergent correction (3 FP64), <= 2 ulp.
 // Arguments are finite positive normals (the coincidence guard keeps 1 - x.y >= 1e-14).
@@ -23,19 +22,17 @@
 namespace csfs_b200 {
 
 // Global table (host-built by make_log_table from log_table.inc): kLogTab double2 {r_i, L_i}.
-// Staged into shared memory per CTA.
+// The evaluation kernels stage it into dynamic shared memory (kLogTabBytes) per CTA.
 struct LogTable {
     const double2* e;  // kLogTab
 };
+constexpr size_t kLogTabBytes = size_t(kLogTab) * sizeof(double2);
 
-struct LogTableSmem {
-    double2 e[kLogTab];
-};
-
-// Copies the global table into shared memory; the caller syncs before use.
-__device__ __forceinline__ LogTable stage_log_table(LogTableSmem& sm, const double2* g) {
-    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) sm.e[i] = g[i];
-    return LogTable{sm.e};
+// Copies the global table into shared memory `sm` (kLogTab entries); the caller syncs
+// before use.
+__device__ __forceinline__ LogTable stage_log_table(double2* sm, const double2* g) {
+    for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) sm[i] = g[i];
+    return LogTable{sm};
 }
 
 constexpr int kLogOff = 0x3fe6a000;              // high word of the lowest m (~0.70703)
@@ -49,10 +46,9 @@ __device__ __forceinline__ double fast_log(double x, const LogTable& tb) {
     const int i = (d >> (20 - kLogTabBits)) & (kLogTab - 1);
     const double m = __hiloint2double(hi - (k << 20), __double2loint(x));
     const double2 e = tb.e[i];
-    // |t| <= 2^-9; exact for the two intervals around m = 1 (r = 1)
+    // |t| <= 2^-11; exact for the two intervals around m = 1 (r = 1)
     const double t = fma(m, e.x, -1.0);
-    double p = -1.0 / 6.0;
-    p = fma(p, t, 1.0 / 5.0);
+    double p = 1.0 / 5.0;
     p = fma(p, t, -1.0 / 4.0);
     p = fma(p, t, 1.0 / 3.0);
     p = fma(p, t, -1.0 / 2.0);

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
     constexpr int D = Op::dim;
     __shared__ double2 sxy[kICH], szw[kICH];
     __shared__ double red[kIB * kTPT * D];
-    __shared__ LogTableSmem tab_sm;
+    extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
     __shared__ int item_sh;
     const int tid = threadIdx.x;
     const LogTable tab = stage_log_table(tab_sm, P.log_tab);  // synced by the loop's first barrier
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op
     __shared__ double2 sxy[kICH], szw[kICH];
     __shared__ double colbuf[kIB / 32][kICH];
     __shared__ double red[kIB * kMTPT];
-    __shared__ LogTableSmem tab_sm;
+    extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
     __shared__ int pair_sh;
     const int tid = threadIdx.x, lane = tid & 31;
     const LogTable tab = stage_log_table(tab_sm, P.log_tab);  // synced by the loop's first barrier
@@ -430,7 +430,7 @@ __global__ void k_direct_items(int n_items, long long nt, int4* item, int nseg) 
 template <class Op>
 __global__ void k_eval_pairs(Op op, const double* x, const double* y, long long n, double* out,
                              const double2* log_tab) {
-    __shared__ LogTableSmem tab_sm;
+    extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
     const LogTable tab = stage_log_table(tab_sm, log_tab);
     __syncthreads();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -441,7 +441,7 @@ __global__ void k_eval_pairs(Op op, const double* x, const double* y, long long 
 }
 
 __global__ void k_eval_math(int fn, const double* x, long long n, double* out, const double2* log_tab) {
-    __shared__ LogTableSmem tab_sm;
+    extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
     const LogTable tab = stage_log_table(tab_sm, log_tab);
     __syncthreads();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -458,12 +458,20 @@ __global__ void k_eval_math(int fn, const double* x, long long n, double* out, c
 }
 
 
+// The evaluation kernels keep the log table in dynamic shared memory; with their static
+// buffers that exceeds the 48 KB default, so opt in once per kernel.
+template <class K>
+void allow_table_smem(K kern) {
+    CSFS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLogTabBytes)));
+}
+
 template <class Op>
 int grid_for(int n_items) {
     int dev = 0, sms = 0, per = 0;
     CSFS_CK(cudaGetDevice(&dev));
     CSFS_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CSFS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interact<Op>, kIB, 0));
+    allow_table_smem(k_interact<Op>);
+    CSFS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interact<Op>, kIB, kLogTabBytes));
     return std::max(1, std::min(n_items, sms * std::max(per, 1)));
 }
 
@@ -471,7 +479,7 @@ template <class Op>
 void launch(const InteractParams& p, const Op& op, cudaStream_t s) {
     if (p.n_items == 0) return;
     CSFS_CK(cudaMemsetAsync(p.counter, 0, sizeof(int), s));
-    k_interact<Op><<<grid_for<Op>(p.n_items), kIB, 0, s>>>(p, op);
+    k_interact<Op><<<grid_for<Op>(p.n_items), kIB, kLogTabBytes, s>>>(p, op);
     CSFS_LAUNCH_CHECK();
 }
 
@@ -483,12 +491,13 @@ void launch_mutual(const MutualParams& m, const Op& op, cudaStream_t s) {
         int dev = 0, sms = 0, per = 0;
         CSFS_CK(cudaGetDevice(&dev));
         CSFS_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CSFS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mutual<Op>, kIB, 0));
+        allow_table_smem(k_mutual<Op>);
+        CSFS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mutual<Op>, kIB, kLogTabBytes));
 #ifndef CSFS_MUTUAL_PERSIST
 #define CSFS_MUTUAL_PERSIST 1
 #endif
         const int grid = CSFS_MUTUAL_PERSIST ? std::max(1, std::min(m.n_pairs, sms * std::max(per, 1))) : m.n_pairs;
-        k_mutual<Op><<<grid, kIB, 0, s>>>(m, op);
+        k_mutual<Op><<<grid, kIB, kLogTabBytes, s>>>(m, op);
         CSFS_LAUNCH_CHECK();
     }
 }
@@ -606,14 +615,14 @@ void eval_pairs(const KernelSpec& k, const double* x, const double* y, long long
                 const double2* log_tab, cudaStream_t s) {
     if (n == 0) return;
     with_op(k, [&](auto op) {
-        k_eval_pairs<<<ceil_div(n, 128), 128, 0, s>>>(op, x, y, n, out, log_tab);
+        k_eval_pairs<<<ceil_div(n, 128), 128, kLogTabBytes, s>>>(op, x, y, n, out, log_tab);
         CSFS_LAUNCH_CHECK();
     });
 }
 
 void eval_math(int fn, const double* x, long long n, double* out, const double2* log_tab, cudaStream_t s) {
     if (n == 0) return;
-    k_eval_math<<<ceil_div(n, 128), 128, 0, s>>>(fn, x, n, out, log_tab);
+    k_eval_math<<<ceil_div(n, 128), 128, kLogTabBytes, s>>>(fn, x, n, out, log_tab);
     CSFS_LAUNCH_CHECK();
 }
 
