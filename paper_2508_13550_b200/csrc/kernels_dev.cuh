@@ -175,8 +175,9 @@ struct OpSalT {
         const double y = rsqrt_seed(__hiloint2double(__double2hiint(omc) + 0x00100000, __double2loint(omc)));
         const double h = omc * y;
         const double eh = fma(-h, y, 0.5);
-        const double r = fma(y, eh * fma(eh, 1.5, 1.0), y);  // y (1 + e/2 + 3e^2/8)
-        const double s = omc * r;                              // gamma/2
+        const double c = eh * fma(eh, 1.5, 1.0);  // e/2 + 3e^2/8
+        const double r = fma(y, c, y);             // y (1 + c) = 1/gamma
+        const double s = fma(h, c, h);             // omc y (1 + c) = gamma/2, off r's chain
         const double L = fast_log(fma(s, s, s), tab);
         return kLogOnly ? L : fma(k, L, r);
     }
