@@ -51,6 +51,16 @@ constexpr int kIB = CSFS_IB;    // threads per CTA
 constexpr int kTPT = CSFS_TPT;  // targets per thread
 constexpr int kICH = 256;       // source points per shared-memory chunk
 constexpr int kUnroll = CSFS_UNROLL;
+// source-loop unroll of k_interact per functor (measured: the log/rsqrt functors gain from
+// deeper unrolling, the larger dilog functor loses): Op::kUnroll, else CSFS_UNROLL
+template <class Op, class = void>
+struct UnrollOf {
+    static constexpr int value = kUnroll;
+};
+template <class Op>
+struct UnrollOf<Op, std::void_t<decltype(Op::kUnroll)>> {
+    static constexpr int value = Op::kUnroll;
+};
 #ifndef CSFS_MTPT
 #define CSFS_MTPT 2
 #endif
@@ -75,6 +85,7 @@ struct InteractParams {
 template <class Op>
 __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, Op op) {
     constexpr int D = Op::dim;
+    constexpr int kU = UnrollOf<Op>::value;
     __shared__ double2 sxy[kICH], szw[kICH];
     __shared__ double red[kIB * kTPT * D];
     extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
@@ -127,7 +138,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
             auto compute = [&](int n, bool guarded) {
                 if (!any) return;
                 if (guarded) {
-#pragma unroll kUnroll
+#pragma unroll kU
                     for (int j = g; j < n; j += G) {
                         const double2 a = sxy[j], b = szw[j];
 #pragma unroll
@@ -135,7 +146,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                             op.template eval<true>(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, acc[k], tab);
                     }
                 } else {
-#pragma unroll kUnroll
+#pragma unroll kU
                     for (int j = g; j < n; j += G) {
                         const double2 a = sxy[j], b = szw[j];
 #pragma unroll

@@ -29,6 +29,7 @@ namespace csfs_b200 {
 // (needs_guard, traverse.cu) — the same values with 5 fewer issue slots per pair.
 struct OpLaplace {
     static constexpr int dim = 1;
+    static constexpr int kUnroll = 16;  // k_interact source-loop unroll
     static constexpr double kSym = 1.0;
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
     template <bool G = true>
@@ -94,6 +95,7 @@ __device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
 
 struct OpBiharmonic {
     static constexpr int dim = 1;
+    static constexpr int kUnroll = 4;
     static constexpr double kSym = 1.0;
     __device__ __forceinline__ double scale() const { return kInv4Pi; }
     template <bool G = true>  // regular at coincidence: no guard either way
@@ -160,6 +162,7 @@ struct OpBiotSavart {
 template <bool kLogOnly>
 struct OpSalT {
     static constexpr int dim = 1;
+    static constexpr int kUnroll = 16;
     static constexpr double kSym = 1.0;
     double scale_, k;
     __host__ static OpSalT make(double pref, double c1, double c2) {
