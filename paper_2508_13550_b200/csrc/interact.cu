@@ -254,8 +254,11 @@ struct MutualParams {
     long long own_b, own_e;
 };
 
+#ifndef CSFS_MMINB
+#define CSFS_MMINB CSFS_MINB
+#endif
 template <class Op>
-__global__ void __launch_bounds__(kIB, CSFS_MINB) k_mutual(MutualParams P, Op op) {
+__global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op op) {
     static_assert(Op::dim == 1, "symmetric path is for scalar kernels");
     __shared__ double2 sxy[kICH], szw[kICH];
     __shared__ double colbuf[kIB / 32][kICH];
