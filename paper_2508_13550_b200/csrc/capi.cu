@@ -20,6 +20,7 @@ struct csfs_b200_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t aux = nullptr;  // the upward pass, overlapped with the dual traversal
+    cudaEvent_t w_copied = nullptr;  // host API: the weights' H2D copy (on aux) is done
     std::string err;
     DeviceTree ttree, stree;
     bool shared = false;
@@ -163,9 +164,11 @@ void prepare_mutual(csfs_b200_ctx* c, cudaStream_t s, bool global) {
     c->items.mutual = c->items.n_partial > 0;
 }
 
+// w_ready: optional event the weights' producer records (the host API copies them on
+// the aux stream while the tree levels are built).
 void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
                const double* sw, size_t ns, const KernelSpec& ks, const FmmConfig& f, double* out,
-               csfs_b200_stats* st, cudaStream_t s) {
+               csfs_b200_stats* st, cudaStream_t s, cudaEvent_t w_ready = nullptr) {
     validate(f, nt, ns);
     c->have_state = false;
     c->have_src_tree = false;
@@ -181,8 +184,8 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     DeviceTree& T = c->ttree;
     DeviceTree& S = c->shared ? c->ttree : c->stree;
     build_tree(T, c->sc, txyz, c->shared ? sw : nullptr, (long long)nt, f.degree, n0, f.shrink,
-               c->cheb, s);
-    if (!c->shared) build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s);
+               c->cheb, s, w_ready);
+    if (!c->shared) build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s, w_ready);
     CSFS_CK(cudaEventRecord(ev[1], s));
 
     // the upward pass (weights -> proxy weights) and the dual traversal (geometry -> lists)
@@ -301,6 +304,7 @@ int csfs_b200_create(csfs_b200_ctx** out, int device) {
                               " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
         CSFS_CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
         CSFS_CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+        CSFS_CK(cudaEventCreateWithFlags(&c->w_copied, cudaEventDisableTiming));
         for (auto& e : c->ev) CSFS_CK(cudaEventCreate(&e));
         CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
         const char* nosym = std::getenv("CSFS_B200_NO_SYMMETRIC");
@@ -330,6 +334,7 @@ void csfs_b200_destroy(csfs_b200_ctx* c) {
     if (c->sc.host) cudaFreeHost(c->sc.host);
     if (c->own) cudaStreamDestroy(c->own);
     if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->w_copied) cudaEventDestroy(c->w_copied);
     delete c;
 }
 
@@ -362,10 +367,13 @@ int csfs_b200_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const doubl
             dsrc = c->h_sxyz.p;
         }
         c->h_w.grow(ns);
-        CSFS_CK(cudaMemcpyAsync(c->h_w.p, sw, ns * sizeof(double), cudaMemcpyHostToDevice, s));
+        // the weights are first needed after the tree levels: copy them on the aux stream
+        // while the positions' tree is built
+        CSFS_CK(cudaMemcpyAsync(c->h_w.p, sw, ns * sizeof(double), cudaMemcpyHostToDevice, c->aux));
+        CSFS_CK(cudaEventRecord(c->w_copied, c->aux));
         const size_t nout = nt * size_t(ks.out_dim());
         c->h_out.grow(nout);
-        run_csfmm(c, c->h_txyz.p, nt, dsrc, c->h_w.p, ns, ks, f, c->h_out.p, st, s);
+        run_csfmm(c, c->h_txyz.p, nt, dsrc, c->h_w.p, ns, ks, f, c->h_out.p, st, s, c->w_copied);
         CSFS_CK(cudaMemcpyAsync(out, c->h_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaStreamSynchronize(s));
     });

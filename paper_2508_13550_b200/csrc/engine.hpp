@@ -170,7 +170,8 @@ struct PhaseTimes {
 
 // tree.cu: builds `tree` from AoS xyz (device, input order) and optional weights.
 void build_tree(DeviceTree& tree, Scratch& sc, const double* xyz, const double* w, long long n,
-                int degree, int n0, bool shrink, const Cheb& cheb, cudaStream_t s);
+                int degree, int n0, bool shrink, const Cheb& cheb, cudaStream_t s,
+                cudaEvent_t w_ready = nullptr);
 // Device byte comparison (targets == sources detection).
 bool device_equal(const void* a, const void* b, size_t bytes, Scratch& sc, cudaStream_t s);
 

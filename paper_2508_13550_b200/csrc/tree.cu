@@ -494,7 +494,8 @@ TreeView DeviceTree::view() const {
 }
 
 void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_in, long long n,
-                int degree, int n0, bool shrink, const Cheb& cheb, cudaStream_t s) {
+                int degree, int n0, bool shrink, const Cheb& cheb, cudaStream_t s,
+                cudaEvent_t w_ready) {
     t.n = n;
     t.degree = degree;
     t.np = degree + 1;
@@ -641,6 +642,8 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
 
     // ---- weights in tree order (permute_weights, summation.cpp:98-104) ---------------------
     if (t.has_w) {
+        // w_ready: the weights' host->device copy, overlapped with the levels above
+        if (w_ready) CSFS_CK(cudaStreamWaitEvent(s, w_ready, 0));
         k_gather<<<gp, kThreads, 0, s>>>(n, t.perm, w_in, t.w);
         CSFS_LAUNCH_CHECK();
     }
