@@ -43,3 +43,27 @@ def test_full_config_parity(engine, name):
     e_r = rel_l2(r[idx], d, wl.areas[idx])
     print(f"{name}: E(FMM, direct) GPU {e_g:.4e} reference {e_r:.4e}")
     assert abs(e_g - e_r) <= 1e-3 * e_r + 1e-12
+
+
+def test_beyond_baseline_size(engine):
+    """Maximum-size case beyond BASELINE.json: the C5 setup at L11 (25,165,824 points, 4x
+    C5).  The reference would take ~10 min on the host, so this one checks what does not
+    need it: the FMM-vs-direct error on sampled targets is that of C5 (same degree and MAC
+    at a finer grid), results are bitwise reproducible run to run, and the list sizes grow
+    ~4x."""
+    wl = configs.make("c5", level=11)
+    cfg = TraversalConfig(mac=wl.mac, degree=wl.degree, n0=wl.n0)
+    k = Kernel.parse(wl.kernel)
+    p = ParticleSet(wl.xyz, wl.weights)
+    st = SumStats()
+    g = engine.csfmm_sum(p, p, k, cfg, st).values
+    g2 = engine.csfmm_sum(p, p, k, cfg).values
+    np.testing.assert_array_equal(g, g2)
+    rng = np.random.default_rng(8)
+    idx = np.sort(rng.choice(wl.n, 4096, replace=False))
+    d = engine.direct_sum(ParticleSet(wl.xyz[idx], np.zeros(idx.size)), p, k).values
+    e = rel_l2(g[idx], d, wl.areas[idx])
+    print(f"c5@L11: N {wl.n}, E(FMM, direct) {e:.4e}, lists {st.pp}/{st.pc}/{st.cp}/{st.cc}, "
+          f"{st.t_total * 1e3:.1f} ms")
+    assert e < 2e-9
+    assert 3.5e6 < st.pp < 4.5e6
