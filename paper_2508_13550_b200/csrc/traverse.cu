@@ -97,31 +97,64 @@ __global__ void k_fill(const int2* __restrict__ l, long long n, int key_off, int
     code[slot] = ((long long)type << 32) | (unsigned)ts.y;
 }
 
-// Per work item: canonical order of its sources, then segment descriptors.
+// Sorts the `n` unique 64-bit codes at c[0, n) ascending with the 32 lanes of a warp: a
+// rank sort (every lane ranks its entries against all, then scatters) for n <= 128, else
+// lane 0 insertion-sorts.  Ends with __syncwarp (the sorted codes are visible warp-wide).
+__device__ __forceinline__ void warp_sort_unique(long long* c, int n, int lane) {
+    constexpr unsigned kFull = 0xffffffffu;
+    if (n <= 128) {
+        long long my[4];
+        int rank[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            my[q] = (lane + 32 * q < n) ? c[lane + 32 * q] : 0;
+            rank[q] = 0;
+        }
+        for (int e = 0; e < n; ++e) {
+            long long v = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const long long vq = __shfl_sync(kFull, my[q], e & 31);
+                if ((e >> 5) == q) v = vq;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rank[q] += (v < my[q]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (lane + 32 * q < n) c[rank[q]] = my[q];
+    } else if (lane == 0) {
+        for (int a = 1; a < n; ++a) {
+            const long long v = c[a];
+            int j = a - 1;
+            while (j >= 0 && c[j] > v) {
+                c[j + 1] = c[j];
+                --j;
+            }
+            c[j + 1] = v;
+        }
+    }
+    __syncwarp();
+}
+
+// Per work item (one warp): canonical order of its sources, then segment descriptors.
 // anchor = first target particle of the item's cluster (owner test for the multi-GPU
 // partition), or -1 for depth-0 targets, which every rank evaluates redundantly.
 __global__ void k_items(int n_items, int ncl_t, const int* __restrict__ keys,
                         const int* __restrict__ cnt, const int* __restrict__ off, long long* code,
                         int2* seg, int4* item, int* anchor, double* cost, const TreeView T,
                         const TreeView S) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_items) return;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (i >= n_items) return;  // warp-uniform
     const int key = keys[i];
     const int b = off[key], n = cnt[key];
     long long* c = code + b;
-    for (int a = 1; a < n; ++a) {  // insertion sort (lists per target are short)
-        const long long v = c[a];
-        int j = a - 1;
-        while (j >= 0 && c[j] > v) {
-            c[j + 1] = c[j];
-            --j;
-        }
-        c[j + 1] = v;
-    }
+    warp_sort_unique(c, n, lane);
     long long src_pts = 0;
     const int t = key < ncl_t ? key : key - ncl_t;
     const bool t_prox = key >= ncl_t;
-    for (int a = 0; a < n; ++a) {
+    for (int a = lane; a < n; a += 32) {
         const int type = int(c[a] >> 32);
         const int s = int(c[a] & 0xffffffffll);
         const bool s_prox = !(type == 0 || type == 2);
@@ -134,11 +167,15 @@ __global__ void k_items(int n_items, int ncl_t, const int* __restrict__ keys,
             src_pts += S.npp;
         }
     }
-    const int tl = key < ncl_t ? T.end[t] - T.begin[t] : T.npp;
-    if (key < ncl_t) item[i] = make_int4(T.begin[t], tl, b, b + n);
-    else item[i] = make_int4(t * T.npp, -T.npp, b, b + n);
-    anchor[i] = T.depth[t] == 0 ? -1 : T.begin[t];
-    cost[i] = double(tl) * double(src_pts);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) src_pts += __shfl_xor_sync(0xffffffffu, src_pts, d);
+    if (lane == 0) {
+        const int tl = key < ncl_t ? T.end[t] - T.begin[t] : T.npp;
+        if (key < ncl_t) item[i] = make_int4(T.begin[t], tl, b, b + n);
+        else item[i] = make_int4(t * T.npp, -T.npp, b, b + n);
+        anchor[i] = T.depth[t] == 0 ? -1 : T.begin[t];
+        cost[i] = double(tl) * double(src_pts);
+    }
 }
 
 __device__ __forceinline__ int unit_of(const long long* ub, int nu, long long b) {
@@ -177,22 +214,21 @@ __global__ void k_mutual_mark(int n_items, int ncl_t, const int* __restrict__ ke
                               const long long* __restrict__ code, int2* seg, int* mflag, int2* epair,
                               const long long* __restrict__ unit_b, int n_units, const TreeView T,
                               unsigned long long* saved) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;  // one warp per item
     unsigned long long sv = 0;
     if (i < n_items) {
         const int key = keys[i];
         const int b = off[key], n = cnt[key];
-        for (int a = 0; a < n; ++a) mflag[b + a] = 0;
+        for (int a = lane; a < n; a += 32) mflag[b + a] = 0;
         const bool leaf_item = key < ncl_t;
         const int t = leaf_item ? key : key - ncl_t;
         const int nt = leaf_item ? T.end[t] - T.begin[t] : T.npp;
         if (T.depth[t] >= 1 && (!leaf_item || nt <= 256)) {
             const int ut = unit_of(unit_b, n_units, T.begin[t]);
             const long long type = leaf_item ? 0 : 3;  // PP entries of leaf items, CC of cluster items
-            for (int a = 0; a < n; ++a) {
+            for (int a = lane; a < n; a += 32) {
                 const long long c = code[b + a];
-                if ((c >> 32) < type) continue;  // sorted by (type, source)
-                if ((c >> 32) > type) break;
+                if ((c >> 32) != type) continue;  // sorted by (type, source)
                 const int s = int(c & 0xffffffffll);
                 const int ns = leaf_item ? T.end[s] - T.begin[s] : T.npp;
                 if (s == t || ns > 256 || T.depth[s] < 1 || unit_of(unit_b, n_units, T.begin[s]) != ut) continue;
@@ -231,18 +267,9 @@ __global__ void k_mutual_fill(int n_pairs, const int4* __restrict__ pair, const 
 }
 
 __global__ void k_mutual_sort(int ncl, const int* __restrict__ mcnt, const int* __restrict__ moff, long long* mlist) {
-    const int X = blockIdx.x * blockDim.x + threadIdx.x;
+    const int X = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;  // one warp per key
     if (X >= ncl) return;
-    long long* l = mlist + moff[X];
-    for (int a = 1; a < mcnt[X]; ++a) {
-        const long long v = l[a];
-        int j = a - 1;
-        while (j >= 0 && l[j] > v) {
-            l[j + 1] = l[j];
-            --j;
-        }
-        l[j + 1] = v;
-    }
+    warp_sort_unique(mlist + moff[X], mcnt[X], lane);
 }
 
 }  // namespace
@@ -286,7 +313,7 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
     CSFS_CK(cudaMemsetAsync(it.pairs.p + 4, 0, sizeof(unsigned long long), s));
     CSFS_CK(cudaMemsetAsync(it.mcnt.p, 0, 2 * ncl * sizeof(int), s));
     CSFS_CK(cudaMemsetAsync(it.mcur.p, 0, 2 * ncl * sizeof(int), s));
-    const int nb = ceil_div(it.n_items, 128);
+    const int nb = ceil_div((long long)it.n_items * 32, 128);
     k_mutual_mark<<<nb, 128, 0, s>>>(it.n_items, ncl, it.keys, it.cnt, it.off, it.code, it.seg, it.mflag, it.epair,
                                      it.unit_b, int(unit_begins.size()), T, it.pairs.p + 4);
     CSFS_LAUNCH_CHECK();
@@ -353,7 +380,7 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
     }
     k_mutual_fill<<<pb, 256, 0, s>>>(it.n_mutual, it.mpair, it.mpoff, it.mleaf, it.moff, it.mcur, it.mlist);
     CSFS_LAUNCH_CHECK();
-    k_mutual_sort<<<ceil_div(2 * ncl, 128), 128, 0, s>>>(2 * ncl, it.mcnt, it.moff, it.mlist);
+    k_mutual_sort<<<ceil_div((long long)2 * ncl * 32, 128), 128, 0, s>>>(2 * ncl, it.mcnt, it.moff, it.mlist);
     CSFS_LAUNCH_CHECK();
 }
 
@@ -470,7 +497,7 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, I
         CSFS_LAUNCH_CHECK();
     }
     if (it.n_items) {
-        k_items<<<ceil_div(it.n_items, 128), 128, 0, s>>>(it.n_items, ncl_t, it.keys, it.cnt, it.off,
+        k_items<<<ceil_div((long long)it.n_items * 32, 128), 128, 0, s>>>(it.n_items, ncl_t, it.keys, it.cnt, it.off,
                                                          it.code, it.seg, it.item, it.anchor, it.cost,
                                                          T, S);
         CSFS_LAUNCH_CHECK();
