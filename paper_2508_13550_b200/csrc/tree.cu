@@ -155,30 +155,66 @@ __device__ __forceinline__ void seg_step(SegAcc<V>& s, int nd, const unsigned lo
     }
 }
 
-// Shrunk bounds: min/max of xi, eta over each new cluster's particles (:53-61).
+// Shrunk bounds: min/max of xi, eta over each new cluster's particles (:53-61).  Each thread
+// first reduces kSegItems CONSECUTIVE particles in registers (a cluster change inside the
+// run flushes with atomics), then the warp combines the per-thread results once; particles
+// of a cluster are contiguous, so most warps see a single cluster for 256 particles.
 __global__ void k_bounds(long long n, int first, const int* nnew_dev, int cnt_host,
                          const int* __restrict__ node, const double* __restrict__ xi,
                          const double* __restrict__ eta, unsigned long long* bnd) {
     const int cnt = nnew_dev ? *nnew_dev : cnt_host;
-    const long long base = (long long)blockIdx.x * blockDim.x * kSegItems + threadIdx.x;
+    const long long base = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kSegItems;
     constexpr int op[4] = {0, 1, 0, 1};
-    SegAcc<4> s;
-    for (int j = 0; j < kSegItems; ++j) {
-        const long long i = base + (long long)j * blockDim.x;
-        int nd = -1;
-        unsigned long long val[4] = {0, 0, 0, 0};
-        if (i < n) {
-            nd = node[i];
-            if (nd >= first && nd < first + cnt) {
-                val[0] = val[1] = ord_enc(xi[i]);
-                val[2] = val[3] = ord_enc(eta[i]);
-            } else {
-                nd = -1;
-            }
+    int cur = -1;
+    unsigned long long acc[4] = {~0ull, 0ull, ~0ull, 0ull};
+    auto flush = [&]() {
+        if (cur >= 0) {
+            atomicMin(&bnd[4ll * cur + 0], acc[0]);
+            atomicMax(&bnd[4ll * cur + 1], acc[1]);
+            atomicMin(&bnd[4ll * cur + 2], acc[2]);
+            atomicMax(&bnd[4ll * cur + 3], acc[3]);
         }
-        seg_step<4>(s, nd, val, bnd, op);
+    };
+    bool mixed = false;  // this thread's run holds more than one cluster
+#pragma unroll
+    for (int j = 0; j < kSegItems; ++j) {
+        const long long i = base + j;
+        if (i >= n) break;
+        int nd = node[i];
+        if (!(nd >= first && nd < first + cnt)) nd = -1;
+        if (nd < 0) continue;
+        const unsigned long long vx = ord_enc(xi[i]), ve = ord_enc(eta[i]);
+        if (nd != cur) {
+            if (cur >= 0) {
+                flush();
+                mixed = true;
+            }
+            cur = nd;
+            acc[0] = acc[1] = vx;
+            acc[2] = acc[3] = ve;
+        } else {
+            acc[0] = vx < acc[0] ? vx : acc[0];
+            acc[1] = vx > acc[1] ? vx : acc[1];
+            acc[2] = ve < acc[2] ? ve : acc[2];
+            acc[3] = ve > acc[3] ? ve : acc[3];
+        }
     }
-    seg_flush<4>(s, bnd, op);
+    // warp combine when every lane ends on the same cluster and none was mixed
+    const int c0 = __shfl_sync(0xffffffffu, cur, 0);
+    if (__all_sync(0xffffffffu, cur == c0 && !mixed)) {
+        if (c0 < 0) return;
+        unsigned long long r[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) r[v] = op[v] ? warp_max_u64(acc[v]) : warp_min_u64(acc[v]);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&bnd[4ll * c0 + 0], r[0]);
+            atomicMax(&bnd[4ll * c0 + 1], r[1]);
+            atomicMin(&bnd[4ll * c0 + 2], r[2]);
+            atomicMax(&bnd[4ll * c0 + 3], r[3]);
+        }
+    } else {
+        flush();
+    }
 }
 
 // Bounds -> interpolant rectangle, centre (:65-66) and the split decision (:95-96).
