@@ -42,6 +42,16 @@ UNIT = "target points/s"
 # Algorithmic FP64 flops per pairwise kernel evaluation (SURVEY.md §8d convention:
 # reference formula as executed by sm_100a libdevice fast paths, DFMA = 2).
 FLOP_PER_PAIR = {"laplace": 53, "sal": 87, "biot_savart": 39, "biharmonic": 94}
+def _hbm_gbs() -> float:
+    """MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth on this pool's B200s)."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6549.4
+
+
+HBM_GBS = _hbm_gbs()
 NOMINAL_FP64_TFLOPS = 37.2
 
 
@@ -284,6 +294,21 @@ def main():
                 "kernel_ms": t_int * 1e3, "share_of_step": t_int / (ms_per_step * 1e-3),
                 "phases_ms": {kk: 1e3 * statistics.mean(getattr(s, kk) for s in stats)
                               for kk in ("t_tree_build", "t_upward", "t_lists", "t_interact", "t_downward", "t_total")}}
+        # the HBM-type phases against the measured copy bandwidth (SURVEY.md §8d algorithmic
+        # bytes): tree build = xyz in (24 B/pt) + per level xi, eta, idx moved (2 x 20 B/pt) +
+        # sorted xyz, w, perm out (36 B/pt); upward leaf = 24 B/pt + (p+1)^2 x 8 B per leaf;
+        # downward leaf = 16 B/pt + 8 dim B/pt.  They are launch/latency-bound small kernels
+        # (4% of the step), reported for completeness.
+        n = wl.n
+        npp = (wl.degree + 1) ** 2
+        hbm_bytes = {"t_tree_build": n * (24 + 40 * s0.tgt_depth + 36),
+                     "t_upward": n * 24 + npp * 8 * s0.src_leaves,
+                     "t_downward": n * (16 + 8 * k.out_dim())}
+        roof["hbm_phases"] = {
+            ph: {"algorithmic_bytes": b, "ms": roof["phases_ms"][ph],
+                 "gbs": b / (roof["phases_ms"][ph] * 1e-3) / 1e9,
+                 "frac_of_hbm": b / (roof["phases_ms"][ph] * 1e-3) / 1e9 / HBM_GBS}
+            for ph, b in hbm_bytes.items()}
 
     # ---- e2e through the host-pointer C-ABI ---------------------------------------------
     e2e = None
