@@ -106,6 +106,7 @@ struct Scratch {
     DevBuf<int> tiles;      // scan tile totals
     DevBuf<int> grand;      // scan grand totals (device)
     DevBuf<int> segP, segE, kid, koff;  // per frontier cluster x 4
+    DevBuf<unsigned long long> qbnd;    // per frontier cluster x 16: quadrant bounds (local levels)
     DevBuf<int> counters;   // misc device counters
     int* host = nullptr;    // pinned host mirror for small read-backs
     DevBuf<double> fxi, feta;  // level-0 face coordinates in input order
