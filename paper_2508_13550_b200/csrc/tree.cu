@@ -12,6 +12,7 @@
 //             order-preserving encodings (exact, so deterministic)   (K4); only xi, eta,
 //             perm and node move between levels
 //   at the end: positions/weights gathered once through perm, every radius in one pass
+//             (a warp per leaf over its ancestors)
 // Internal cluster ids are level-major (BFS); reference_ids() maps them onto the
 // reference's LIFO numbering for export (K5).  Particle data stays SoA in HBM.
 #include <algorithm>
@@ -254,50 +255,32 @@ __global__ void k_geom(int first, const int* nnew_dev, int cnt_host, ClusterPtrs
     if (sp) atomicAdd(nsplit, 1);
 }
 
-// Radii of every cluster once the tree is final (:67-69): positions are gathered into tree
-// order once, and each particle visits its ancestors level by level (deepest first);
-// kSegItems particles per thread keep their positions and current ancestor in registers.
-__global__ void k_radius_all(long long n, int max_depth, const int* __restrict__ node,
-                             const int* __restrict__ depth, const int* __restrict__ parent,
-                             const double* __restrict__ px, const double* __restrict__ py,
-                             const double* __restrict__ pz, const double* __restrict__ cx,
-                             const double* __restrict__ cy, const double* __restrict__ cz, double* rad) {
-    const long long base = (long long)blockIdx.x * blockDim.x * kSegItems + threadIdx.x;
-    constexpr int op[1] = {1};
+// Radii of every cluster once the tree is final (:67-69), by leaf: one warp per leaf computes its particles' chordal distances to the leaf's
+// centre and to every ancestor's, reduces each over the warp and max-es it into the
+// ancestor (integer atomics on the bit patterns of non-negative doubles: exact, order
+// independent).  Positions are read once per leaf (re-reads hit L1); the same distances
+// and maxima as a per-particle walk, with one atomic per (leaf, ancestor).
+__global__ void k_radius_leaf(int ncl, const int* __restrict__ nchild, const int* __restrict__ begin,
+                              const int* __restrict__ end, const int* __restrict__ parent,
+                              const double* __restrict__ px, const double* __restrict__ py,
+                              const double* __restrict__ pz, const double* __restrict__ cx,
+                              const double* __restrict__ cy, const double* __restrict__ cz, double* rad) {
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (c >= ncl || nchild[c] > 0) return;  // warp-uniform
+    const int b = begin[c], e = end[c];
     unsigned long long* radu = reinterpret_cast<unsigned long long*>(rad);
-    double x[kSegItems], y[kSegItems], z[kSegItems];
-    int a[kSegItems];
-#pragma unroll
-    for (int j = 0; j < kSegItems; ++j) {
-        const long long i = base + (long long)j * blockDim.x;
-        a[j] = -1;
-        x[j] = y[j] = z[j] = 0.0;
-        if (i < n) {
-            a[j] = node[i];
-            x[j] = px[i];
-            y[j] = py[i];
-            z[j] = pz[i];
+    for (int a = c; a >= 0; a = parent[a]) {
+        const double ax = cx[a], ay = cy[a], az = cz[a];
+        unsigned long long m = 0;
+        for (int i = b + lane; i < e; i += 32) {
+            const double dx = __dsub_rn(ax, px[i]);
+            const double dy = __dsub_rn(ay, py[i]);
+            const double dz = __dsub_rn(az, pz[i]);
+            const unsigned long long v = __double_as_longlong(__dsqrt_rn(dot_ref(dx, dy, dz, dx, dy, dz)));
+            m = v > m ? v : m;
         }
-    }
-    for (int L = max_depth; L >= 0; --L) {
-        SegAcc<1> s;
-#pragma unroll
-        for (int j = 0; j < kSegItems; ++j) {
-            int nd = -1;
-            unsigned long long val[1] = {0};
-            if (a[j] >= 0) {
-                while (depth[a[j]] > L) a[j] = parent[a[j]];
-                if (depth[a[j]] == L) {
-                    nd = a[j];
-                    const double dx = __dsub_rn(cx[nd], x[j]);
-                    const double dy = __dsub_rn(cy[nd], y[j]);
-                    const double dz = __dsub_rn(cz[nd], z[j]);
-                    val[0] = __double_as_longlong(__dsqrt_rn(dot_ref(dx, dy, dz, dx, dy, dz)));
-                }
-            }
-            seg_step<1>(s, nd, val, radu, op);
-        }
-        seg_flush<1>(s, radu, op);
+        m = warp_max_u64(m);
+        if (lane == 0 && b < e) atomicMax(&radu[a], m);
     }
 }
 
@@ -621,7 +604,7 @@ void finish_level(DeviceTree& t, Scratch& sc, int first, const int* nnew_dev, in
     CSFS_CK(cudaMemsetAsync(sc.counters.p + 1, 0, sizeof(int), s));
     k_geom<<<gb, kThreads, 0, s>>>(first, nnew_dev, cnt_bound, c, t.shrink, t.n0, sc.counters.p + 1);
     CSFS_LAUNCH_CHECK();
-// radii: once for all levels after the build (k_radius_all)
+// radii: once for all levels after the build (k_radius_leaf)
 }
 
 template <class T>
@@ -881,8 +864,8 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
     // ---- positions in tree order, then every cluster's radius ------------------------------
     k_gather_xyz<<<gp, kThreads, 0, s>>>(n, t.perm, xyz, t.px, t.py, t.pz);
     CSFS_LAUNCH_CHECK();
-    k_radius_all<<<ceil_div(n, kThreads * kSegItems), kThreads, 0, s>>>(n, t.depth_max(), t.node, t.depth, t.parent,
-                                                                       t.px, t.py, t.pz, t.cx, t.cy, t.cz, t.rad);
+    k_radius_leaf<<<ceil_div((long long)t.ncl * 32, 128), 128, 0, s>>>(t.ncl, t.nchild, t.begin, t.end, t.parent,
+                                                                      t.px, t.py, t.pz, t.cx, t.cy, t.cz, t.rad);
     CSFS_LAUNCH_CHECK();
 
     // ---- weights in tree order (permute_weights, summation.cpp:98-104) ---------------------
