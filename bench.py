@@ -103,7 +103,8 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (wall time, csv line)
+        self.window = None  # (t0, t1): keep the samples taken inside the timed region
 
     def __enter__(self):
         try:
@@ -118,7 +119,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def start(self):
+        """nvidia-smi takes ~0.5 s to deliver its first sample: start it before the warm-up."""
+        return self.__enter__()
+
+    def mark(self, t0: float, t1: float):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -130,7 +138,11 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        for ln in self.lines:
+        lines = self.lines
+        if self.window is not None:
+            inside = [x for x in lines if self.window[0] <= x[0] <= self.window[1] + 0.1]
+            lines = inside if inside else lines[-1:]
+        for _, ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -233,9 +245,10 @@ def main():
         if part:
             dist.barrier()
 
+    fp64_peak = eng.probe_fp64_tflops()
+    clk = ClockSampler(local).start()  # running through the warm-up; samples kept for the timed region
     for _ in range(args.warmup):
         step()
-    fp64_peak = eng.probe_fp64_tflops()
 
     # ---- timed: device-resident (value) -------------------------------------------------
     stats = []
@@ -243,14 +256,16 @@ def main():
     torch.cuda.synchronize()
     l0 = kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            st = SumStats()
-            step(st)
-            stats.append(st)
-        e1.record(stream)
-        torch.cuda.synchronize()
+    t_wall0 = time.time()
+    e0.record(stream)
+    for _ in range(args.steps):
+        st = SumStats()
+        step(st)
+        stats.append(st)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk.mark(t_wall0, time.time())
+    clk.__exit__(None, None, None)
     barrier()
     launches = kernel_launches() - l0
     ms = e0.elapsed_time(e1)
