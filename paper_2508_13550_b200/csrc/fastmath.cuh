@@ -6,12 +6,14 @@
 //            m in [0.7070, 1.4141) (so both sides of x = 1 have k = 0), m r_i = 1 + t,
 //            |t| <= 2^-11, from a 2048-entry table of {r_i, L_i} (32 KB, dynamic shared
 //            memory): r_i is chosen near 1/centre_i so that L_i = -ln r_i is within 2^-67
-//            of the 2^-46 grid (tools/gen_log_table.c), hence k ln2_hi + L_i is exact in
-//            one FMA and no low-order table word is needed: one LDS.128 per lookup.  The two
-//            intervals around 1 use r = 1, L = 0, so t = m - 1 is exact and log keeps full
-//            relative accuracy where log(x) ~ 0 — branch-free.  log1p(t) by a degree-5
-//            polynomial.  9 FP64 instructions (+ one int->double conversion on the XU pipe),
-//            <= 1 ulp (mpmath check in tests/test_gpu_numerics.py).  Domain: positive normals.
+//            of the 2^-46 grid (tools/gen_log_table.c): one LDS.128 per lookup.  The two
+//            intervals around 1 use r = 1, L = 0, so t = m - 1 is exact — branch-free.
+//            k ln2 + L_i in one FMA, log1p(t) by a degree-4 polynomial: 7 FP64
+//            instructions (+ one int->double conversion).  Error <= 1 ulp + |t|^5/5
+//            (<= 5.6e-18 absolute, reached only in the interval just above 1, where the value
+//            is ~t: up to ~100 ulp RELATIVE there); the kernels add log to O(1) terms, so
+//            only the absolute error reaches them (tests/test_gpu_numerics.py).  Domain:
+//            positive normals.
 //   rsqrt -> MUFU.RSQ64H seed + one cubic-convergent correction (5 FP64), <= 2 ulp.
 //   rcp   -> MUFU.RCP64H seed + one cubic-convergent correction (3 FP64), <= 2 ulp.
 // Arguments are finite positive normals (the coincidence guard keeps 1 - x.y >= 1e-14).
@@ -36,8 +38,7 @@ __device__ __forceinline__ LogTable stage_log_table(double2* sm, const double2* 
 }
 
 constexpr int kLogOff = 0x3fe6a000;              // high word of the lowest m (~0.70703)
-constexpr double kLn2Hi = 0x1.62e42fefa3800p-1;  // 42 significant bits: k*kLn2Hi exact
-constexpr double kLn2Lo = 0x1.ef35793c76730p-45;
+constexpr double kLn2 = 0x1.62e42fefa39efp-1;
 
 __device__ __forceinline__ double fast_log(double x, const LogTable& tb) {
     const int hi = __double2hiint(x);
@@ -48,14 +49,10 @@ __device__ __forceinline__ double fast_log(double x, const LogTable& tb) {
     const double2 e = tb.e[i];
     // |t| <= 2^-11; exact for the two intervals around m = 1 (r = 1)
     const double t = fma(m, e.x, -1.0);
-    double p = 1.0 / 5.0;
-    p = fma(p, t, -1.0 / 4.0);
-    p = fma(p, t, 1.0 / 3.0);
-    p = fma(p, t, -1.0 / 2.0);
-    const double kd = double(k);
-    const double A = fma(kd, kLn2Hi, e.y);  // exact: multiples of 2^-46, |A| < 128
-    const double B = fma(kd, kLn2Lo, t);    // == t where k == 0
-    return A + fma(t * t, p, B);
+    const double p = fma(fma(-1.0 / 4.0, t, 1.0 / 3.0), t, -1.0 / 2.0);
+    // k ln2 + L_i in one FMA (k ln2 rounded once inside it; |k| <= 1 for most arguments)
+    const double A = fma(double(k), kLn2, e.y);
+    return A + fma(t * t, p, t);
 }
 
 __device__ __forceinline__ double rsqrt_seed(double x) {

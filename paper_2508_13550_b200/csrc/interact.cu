@@ -304,9 +304,9 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
         for (int k = 0; k < kMTPT; ++k) {
             const int t = r + k * gs;
             act[k] = grp && t < tlen;
-            tx[k] = 0.0;
-            ty[k] = 0.0;
-            tz[k] = 1.0;
+            tx[k] = 0.0;  // padding target at the origin: 1 - x.y = 1 for every source, so its
+            ty[k] = 0.0;  // (zero-weight) column terms stay finite in the unguarded path
+            tz[k] = 0.0;
             tw[k] = 0.0;
             if (act[k]) {
                 tx[k] = X[q.x + t];
