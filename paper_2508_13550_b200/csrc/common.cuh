@@ -79,6 +79,11 @@ __device__ __forceinline__ bool not_coincident(double omc) {
     return __double_as_longlong(omc) >= __double_as_longlong(kCoincidenceTol);
 }
 
+// The same test on hom = omc / 2 (exact: functors that take halved targets, OpSalT).
+__device__ __forceinline__ bool not_coincident_half(double hom) {
+    return __double_as_longlong(hom) >= __double_as_longlong(0.5 * kCoincidenceTol);
+}
+
 // `ok ? omc : (a value in [1, 1 + 2^-20))` with a single 32-bit select: the skipped pair
 // only needs a safe finite argument for the log / rsqrt / rcp that follow.
 __device__ __forceinline__ double safe_omc(bool ok, double omc) {

@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(kCstcThreads)
     if (idx < nt) {
         const long long i = order ? order[idx] : idx;
         const double x = txyz[3 * i], y = txyz[3 * i + 1], z = txyz[3 * i + 2];
+        const double tx = op.tgt(x), ty = op.tgt(y), tz = op.tgt(z);  // the functor's target form
         double acc[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) acc[d] = 0.0;
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(kCstcThreads)
             if (sep) {
                 if (e - b > n0) {
                     const long long q0 = (long long)s * npp;
-                    for (int k = 0; k < npp; ++k) op(x, y, z, S.qx[q0 + k], S.qy[q0 + k], S.qz[q0 + k], qw[q0 + k], acc, tab);
+                    for (int k = 0; k < npp; ++k) op(tx, ty, tz, S.qx[q0 + k], S.qy[q0 + k], S.qz[q0 + k], qw[q0 + k], acc, tab);
                     ++npc;
                     continue;
                 }
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(kCstcThreads)
                 for (int q = 0; q < S.nchild[s] && sp < kStack; ++q) stack[sp++] = cs[q];
                 continue;
             }
-            for (int j = b; j < e; ++j) op(x, y, z, S.px[j], S.py[j], S.pz[j], sw[j], acc, tab);
+            for (int j = b; j < e; ++j) op(tx, ty, tz, S.px[j], S.py[j], S.pz[j], sw[j], acc, tab);
             ++npp_;
         }
         const double sc = op.scale();

@@ -126,9 +126,9 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                 ty[k] = 0.0;
                 tz[k] = 1.0;
                 if (act[k]) {
-                    tx[k] = TX[d.x + t];
-                    ty[k] = TY[d.x + t];
-                    tz[k] = TZ[d.x + t];
+                    tx[k] = op.tgt(TX[d.x + t]);
+                    ty[k] = op.tgt(TY[d.x + t]);
+                    tz[k] = op.tgt(TZ[d.x + t]);
                 }
 #pragma unroll
                 for (int c = 0; c < D; ++c) acc[k][c] = 0.0;
@@ -309,9 +309,9 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
             tz[k] = 0.0;
             tw[k] = 0.0;
             if (act[k]) {
-                tx[k] = X[q.x + t];
-                ty[k] = Y[q.x + t];
-                tz[k] = Z[q.x + t];
+                tx[k] = op.tgt(X[q.x + t]);
+                ty[k] = op.tgt(Y[q.x + t]);
+                tz[k] = op.tgt(Z[q.x + t]);
                 tw[k] = Wt[q.x + t];
             }
             acc[k] = 0.0;
@@ -450,7 +450,7 @@ __global__ void k_eval_pairs(Op op, const double* x, const double* y, long long 
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc[3] = {0.0, 0.0, 0.0};
-    op(x[3 * i], x[3 * i + 1], x[3 * i + 2], y[3 * i], y[3 * i + 1], y[3 * i + 2], 1.0, acc, tab);
+    op(op.tgt(x[3 * i]), op.tgt(x[3 * i + 1]), op.tgt(x[3 * i + 2]), y[3 * i], y[3 * i + 1], y[3 * i + 2], 1.0, acc, tab);
     for (int c = 0; c < Op::dim; ++c) out[i * Op::dim + c] = acc[c] * op.scale();
 }
 

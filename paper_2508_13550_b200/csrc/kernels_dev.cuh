@@ -12,8 +12,9 @@
 //  * the prefactor (-1/4pi, 1/4pi, 3 rho/4pi) is applied once per target (`scale`);
 //  * log / rsqrt / rcp come from fastmath.cuh (11 / 5 / 3 FP64 instructions instead of
 //    libdevice's ~28 / 8+8 / 8), each within a few ulp;
-//  * SAL: 1/gamma = rsqrt(2 omc), s = gamma/2 = omc * rsqrt(2 omc) (halving is exact),
-//    log(s (1 + s)) = log(fma(s, s, s)) — the reference's formula, without sqrt or divide.
+//  * SAL: targets enter halved, so 0.5 - t'.s = omc/2 exactly; 2/gamma = rsqrt(omc/2),
+//    s = gamma/2 = (omc/2) rsqrt(omc/2), log(s (1 + s)) = log(fma(s, s, s)) — the
+//    reference's formula, without sqrt, divide or a seed rescale.
 #pragma once
 
 #include "common.cuh"
@@ -31,6 +32,7 @@ struct OpLaplace {
     static constexpr int dim = 1;
     static constexpr int kUnroll = 16;  // k_interact source-loop unroll
     static constexpr double kSym = 1.0;
+    __device__ __forceinline__ static double tgt(double x) { return x; }
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
     template <bool G = true>
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
@@ -97,6 +99,7 @@ struct OpBiharmonic {
     static constexpr int dim = 1;
     static constexpr int kUnroll = 4;
     static constexpr double kSym = 1.0;
+    __device__ __forceinline__ static double tgt(double x) { return x; }
     __device__ __forceinline__ double scale() const { return kInv4Pi; }
     template <bool G = true>  // regular at coincidence: no guard either way
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
@@ -123,6 +126,7 @@ struct OpBiharmonic {
 struct OpBiotSavart {
     static constexpr int dim = 3;
     static constexpr double kSym = -1.0;  // cross(s, t) = -cross(t, s), 1 - s.t = 1 - t.s
+    __device__ __forceinline__ static double tgt(double x) { return x; }
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
     template <bool G = true>
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
@@ -157,8 +161,9 @@ struct OpBiotSavart {
 
 // SalOp (summation.cpp:63-76): pref (c1/gamma - c2 log(s (1 + s))), gamma = sqrt(2 omc),
 // s = gamma/2.  The constant c1 is folded into scale() (one FMA per pair instead of a
-// multiply and an FMA): K' = 1/gamma + k log(s (1 + s)), k = -c2/c1, scale = pref c1.  The
-// c1 == 0 case (pure log kernel) is the kLogOnly instantiation: K' = log(...), scale = -pref c2.
+// multiply and an FMA): K' = 2/gamma + k log(s (1 + s)), k = -2 c2/c1, scale = pref c1 / 2
+// (the factor 2 comes from the halved targets, below).  The c1 == 0 case (pure log
+// kernel) is the kLogOnly instantiation: K' = log(...), scale = -pref c2.
 template <bool kLogOnly>
 struct OpSalT {
     static constexpr int dim = 1;
@@ -167,37 +172,43 @@ struct OpSalT {
     double scale_, k;
     __host__ static OpSalT make(double pref, double c1, double c2) {
         OpSalT op;
-        op.scale_ = kLogOnly ? -pref * c2 : pref * c1;
-        op.k = kLogOnly ? 0.0 : -c2 / c1;
+        op.scale_ = kLogOnly ? -pref * c2 : 0.5 * (pref * c1);
+        op.k = kLogOnly ? 0.0 : -2.0 * (c2 / c1);
         return op;
     }
     __device__ __forceinline__ double scale() const { return scale_; }
-    // r = 1/gamma: MUFU seed of 2 omc (exponent + 1 on the integer pipe), then the cubic
-    // correction written on omc itself: e/2 = 1/2 - omc y^2 (no FP64 doubling).
-    __device__ __forceinline__ double kernel(double omc, const LogTable& tab) const {
-        const double y = rsqrt_seed(__hiloint2double(__double2hiint(omc) + 0x00100000, __double2loint(omc)));
-        const double h = omc * y;
-        const double eh = fma(-h, y, 0.5);
-        const double c = eh * fma(eh, 1.5, 1.0);  // e/2 + 3e^2/8
-        const double r = fma(y, c, y);             // y (1 + c) = 1/gamma
-        const double s = fma(h, c, h);             // omc y (1 + c) = gamma/2, off r's chain
+    // Targets enter halved (exact): every product of the dot, the dot itself and
+    // hom = 0.5 - t'.s are then exactly half of the reference's, so hom = omc/2 bit for bit
+    // and the guard compares it with 1e-14/2.  The MUFU seed is taken on hom directly:
+    // y ~ 1/sqrt(hom) = 2/gamma.
+    __device__ __forceinline__ static double tgt(double x) { return 0.5 * x; }
+    // 2/gamma and log(s (1 + s)), s = gamma/2 = sqrt(hom): cubic correction of the seed,
+    // e = 1 - hom y^2, c = e/2 + 3e^2/8, 2/gamma = y (1 + c), s = hom y (1 + c).  Returns
+    // 2/gamma + 2k log(...) (scale() carries the 1/2), or the log alone.
+    __device__ __forceinline__ double kernel(double hom, const LogTable& tab) const {
+        const double y = rsqrt_seed(hom);
+        const double h = hom * y;
+        const double e = fma(-h, y, 1.0);
+        const double c = e * fma(e, 0.375, 0.5);
+        const double r2 = fma(y, c, y);  // 2/gamma
+        const double s = fma(h, c, h);   // gamma/2, off r2's chain
         const double L = fast_log(fma(s, s, s), tab);
-        return kLogOnly ? L : fma(k, L, r);
+        return kLogOnly ? L : fma(k, L, r2);
     }
     template <bool G = true>
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
-        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = !G || not_coincident(omc);
-        const double v = kernel(G ? safe_omc(ok, omc) : omc, tab);
+        const double hom = __dsub_rn(0.5, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = !G || not_coincident_half(hom);
+        const double v = kernel(G ? safe_omc(ok, hom) : hom, tab);
         K[0] = ok ? v : 0.0;
     }
     template <bool G = true>
     __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
                                          double* acc, const LogTable& tab) const {
-        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
-        const bool ok = !G || not_coincident(omc);
-        const double v = kernel(G ? safe_omc(ok, omc) : omc, tab);
+        const double hom = __dsub_rn(0.5, dot_ref(tx, ty, tz, sx, sy, sz));
+        const bool ok = !G || not_coincident_half(hom);
+        const double v = kernel(G ? safe_omc(ok, hom) : hom, tab);
         acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
     }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
