@@ -237,9 +237,10 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
 // evaluated ONCE and applied to both sides — row sums to A, column sums to B
 // (K(b, a) = kSym K(a, b) bit-for-bit).  Same register/shared-memory structure as
 // k_interact: A's targets (kTPT per thread) and their weights in registers, B (<= 256
-// points) in shared memory, G thread groups splitting B.  Column partials are reduced per
-// warp with a transposed butterfly over source pairs (5 shuffle steps per 2 sources), then
-// over the group's warps in fixed order: deterministic, no atomics.  Both partial sums go
+// points) in shared memory, G thread groups splitting B in batches of 8.  Column partials
+// are reduced per warp with a select-free transposed butterfly (4+2+1+1+1 shuffles per 8
+// sources, each lane visiting the batch in its own XOR order), then over the group's warps
+// in fixed order: deterministic, no atomics.  Both partial sums go
 // to `partial`; k_mutual_reduce adds them to phi_near after the list items.
 struct MutualParams {
     const int4* pair;       // {A begin, |A|, B begin, |B|}, |A|, |B| <= 256; negative: proxy sets (CC)
@@ -253,6 +254,14 @@ struct MutualParams {
     const double2* log_tab;
     long long own_b, own_e;
 };
+
+// double butterfly shuffle as two explicit 32-bit halves (keeps the halves in place; the
+// generic double overload let ptxas swap them and re-pair with moves)
+__device__ __forceinline__ double shfl_xor_d(double v, int m) {
+    const int lo = __shfl_xor_sync(0xffffffffu, __double2loint(v), m);
+    const int hi = __shfl_xor_sync(0xffffffffu, __double2hiint(v), m);
+    return __hiloint2double(hi, lo);
+}
 
 #ifndef CSFS_MMINB
 #define CSFS_MMINB CSFS_MINB
@@ -289,9 +298,11 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
         const double* Z = prox ? P.qz : P.pz;
         const double* Wt = prox ? P.qw : P.pw;
         const int tlen = seg_len(q.y), nb = seg_len(q.w);
-        for (int j = tid; j < nb; j += kIB) {
-            sxy[j] = make_double2(X[q.z + j], Y[q.z + j]);
-            szw[j] = make_double2(Z[q.z + j], Wt[q.z + j]);
+        // padded to whole batches of 8 with zero-weight sources at the origin (finite K)
+        for (int j = tid; j < ((nb + 7) & ~7); j += kIB) {
+            const bool in = j < nb;
+            sxy[j] = in ? make_double2(X[q.z + j], Y[q.z + j]) : make_double2(0.0, 0.0);
+            szw[j] = in ? make_double2(Z[q.z + j], Wt[q.z + j]) : make_double2(0.0, 0.0);
         }
         const int per = (tlen + kMTPT - 1) / kMTPT;
         const int gs = min(kIB, (per + 31) & ~31);
@@ -318,56 +329,41 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
         }
         __syncthreads();
         if (grp) {
-            // 8 sources (j + m*G, m < 8) per step; their per-thread column partials are reduced
-            // over the warp by a transposed butterfly: 4+2+1+1+1 shuffles for 8 sources
+            // Batches of 8 consecutive sources, batch t to group t mod G.  Lane slot s holds
+            // source s ^ q, q = (lane >> 2) & 7: the transposed butterfly then always keeps
+            // the low half of its slots (no selects) and ends with lane holding source q's
+            // column sum over the warp.  The 8 per-lane addresses of a slot are 8
+            // consecutive entries: one shared-memory wavefront.
             constexpr int kB = 8;
-            const int full_end = nb - (kB - 1) * G;  // j < full_end: all 8 sources exist
-            // tail: the last batch may be short; kG: the coincidence guard (pair-uniform)
-            auto sources = [&](int j, double (&c)[kB], bool tail, auto kG) {
+            const int qx = (lane >> 2) & 7;
+            auto sources = [&](int j, double (&c)[kB], auto kG) {
 #pragma unroll
                 for (int m = 0; m < kB; ++m) {
                     c[m] = 0.0;
-                    const int jm = j + m * G;
-                    if (!tail || jm < nb) {  // group-uniform
-                        const double2 a = sxy[jm], b = szw[jm];
+                    const int jm = j + (m ^ qx);
+                    const double2 a = sxy[jm], b = szw[jm];
 #pragma unroll
-                        for (int k = 0; k < kMTPT; ++k) {
-                            double K[1];
-                            op.template value<decltype(kG)::value>(tx[k], ty[k], tz[k], a.x, a.y, b.x, K, tab);
-                            acc[k] = fma(b.y, K[0], acc[k]);
-                            c[m] = fma(tw[k], K[0], c[m]);
-                        }
+                    for (int k = 0; k < kMTPT; ++k) {
+                        double K[1];
+                        op.template value<decltype(kG)::value>(tx[k], ty[k], tz[k], a.x, a.y, b.x, K, tab);
+                        acc[k] = fma(b.y, K[0], acc[k]);
+                        c[m] = fma(tw[k], K[0], c[m]);
                     }
                 }
             };
-            for (int j = g; j < nb; j += kB * G) {
+            for (int j = g * kB; j < nb; j += kB * G) {
                 double c[kB];
-                if (guarded) {
-                    if (j < full_end) sources(j, c, false, std::true_type{});
-                    else sources(j, c, true, std::true_type{});
-                } else {
-                    if (j < full_end) sources(j, c, false, std::false_type{});
-                    else sources(j, c, true, std::false_type{});
-                }
-                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                if (guarded) sources(j, c, std::true_type{});
+                else sources(j, c, std::false_type{});
                 double v4[4], v2[2];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {  // lanes < 16 keep sources 0..3, >= 16 keep 4..7
-                    const double keep = b4 ? c[m + 4] : c[m];
-                    const double send = b4 ? c[m] : c[m + 4];
-                    v4[m] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                }
+                for (int m = 0; m < 4; ++m) v4[m] = c[m] + shfl_xor_d(c[m + 4], 16);
 #pragma unroll
-                for (int m = 0; m < 2; ++m) {
-                    const double keep = b3 ? v4[m + 2] : v4[m];
-                    const double send = b3 ? v4[m] : v4[m + 2];
-                    v2[m] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                }
-                double v = (b2 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? v2[0] : v2[1], 4);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                const int m = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
-                const int jm = j + m * G;
+                for (int m = 0; m < 2; ++m) v2[m] = v4[m] + shfl_xor_d(v4[m + 2], 8);
+                double v = v2[0] + shfl_xor_d(v2[1], 4);
+                v += shfl_xor_d(v, 2);
+                v += shfl_xor_d(v, 1);
+                const int jm = j + qx;
                 if ((lane & 3) == 0 && jm < nb) colbuf[wig][jm] = v;
             }
         }
@@ -389,7 +385,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
             for (int k = 0; k < kMTPT; ++k)
                 if (act[k]) P.partial[base + r + k * gs] = acc[k] * op.scale();
         }
-        // columns: source j was handled by group j % G, whose warps wrote colbuf[0..W)[j]
+        // columns: source j was handled by one group, whose warps wrote colbuf[0..W)[j]
         const int W = gs >> 5;
         const double f = op.scale() * Op::kSym;
         for (int j = tid; j < nb; j += kIB) {
