@@ -135,11 +135,15 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
             }
             const bool any = act[0];  // slot 0 is filled first
             // guarded: the chunk holds a segment that may contain coincident pairs
+            // group g takes a contiguous share of the chunk: unit stride, so the unrolled
+            // loop addresses shared memory with immediate offsets (no per-source pointer math)
             auto compute = [&](int n, bool guarded) {
                 if (!any) return;
+                const int share = (n + G - 1) / G;
+                const int jb = g * share, je = min(n, jb + share);
                 if (guarded) {
 #pragma unroll kU
-                    for (int j = g; j < n; j += G) {
+                    for (int j = jb; j < je; ++j) {
                         const double2 a = sxy[j], b = szw[j];
 #pragma unroll
                         for (int k = 0; k < kTPT; ++k)
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                     }
                 } else {
 #pragma unroll kU
-                    for (int j = g; j < n; j += G) {
+                    for (int j = jb; j < je; ++j) {
                         const double2 a = sxy[j], b = szw[j];
 #pragma unroll
                         for (int k = 0; k < kTPT; ++k)
