@@ -273,7 +273,9 @@ __device__ __forceinline__ double shfl_xor_d(double v, int m) {
 template <class Op>
 __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op op) {
     static_assert(Op::dim == 1, "symmetric path is for scalar kernels");
-    __shared__ double2 sxy[kICH], szw[kICH];
+    __shared__ double2 sbuf[2 * kICH];  // {x,y} then {z,w}: one base register, immediate offset
+    double2* const sxy = sbuf;
+    double2* const szw = sbuf + kICH;
     __shared__ double colbuf[kIB / 32][kICH];
     __shared__ double red[kIB * kMTPT];
     extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
