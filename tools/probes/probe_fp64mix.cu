@@ -19,6 +19,11 @@ __global__ void __launch_bounds__(256) k_mix(double* sink, int iters, double a, 
                 asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x[c]));
                 x[c] = fma(fma(fma(fma(fma(fma(fma(x[c], a, b), a, b), a, b), a, b), a, b), a, b), a, y * 1e-30);
             }
+            if (MODE == 5 || MODE == 6) {  // 7 DFMA + SHF + (I2F.F64 | LOP3): is I2F.F64 an FP64-pipe op?
+                const int k = __double2hiint(x[c]) >> 20;
+                const double dk = MODE == 5 ? double(k) : __hiloint2double(k | 0x3ff00000, 0);
+                x[c] = fma(fma(fma(fma(fma(fma(fma(x[c], a, b), a, b), a, b), a, b), a, b), a, b), a, dk);
+            }
         }
     }
     double s = 0.0;
@@ -54,5 +59,7 @@ int main() {
     run<2>("DADD", 1, sink);
     run<3>("DFMA/DMUL/DADD mix", 1, sink);
     run<4>("7 DFMA + 1 RSQ64H + DMUL", 8, sink);
+    run<5>("7 DFMA + SHF + I2F.F64", 7, sink);
+    run<6>("7 DFMA + SHF + LOP3", 7, sink);
     return 0;
 }
