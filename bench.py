@@ -184,7 +184,7 @@ def run_reference(args):
             "data": "synthetic", "config": workload_config(wl),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -196,7 +196,24 @@ def workload_config(wl):
             "l2": "inputs (N x 32 B = 201 MB) and proxy/potential arrays exceed the 126 MB L2; no flush"}
 
 
+_OUT_FD = None  # the real stdout; fd 1 points at stderr while the run prints (NCCL banners, ...)
+
+
+def emit(line):
+    """The ONE JSON line, on the real stdout (everything else the run prints went to stderr)."""
+    data = (json.dumps(line) + "\n").encode()
+    if _OUT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_OUT_FD, data)
+
+
 def main():
+    global _OUT_FD
+    sys.stdout.flush()
+    _OUT_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -379,7 +396,7 @@ def main():
         if roof:
             line["fp64_frac_p2p_m2l"] = roof["frac"]
             line["fp64_frac_p2p_m2l_executed"] = roof["executed_frac"]
-        print(json.dumps(line), flush=True)
+        emit(line)
     if part:
         dist.destroy_process_group()
     eng.close()

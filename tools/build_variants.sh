@@ -3,7 +3,7 @@
 set -e
 cd "$(dirname "$0")/.."
 for v in "$@"; do
-  name=$(echo "$v" | tr ' =' '_-')
+  name=$(echo "$v" | sed 's/-DCSFS_//g' | tr ' =' '_-')
   out=_variants/$name
   mkdir -p $out/obj
   make -s -C paper_2508_13550_b200/csrc OUT=$PWD/$out/libcsfs_b200.so OBJ=$PWD/$out/obj EXTRA_NVFLAGS="$v" -j8 >/dev/null

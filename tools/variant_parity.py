@@ -1,7 +1,7 @@
 """Developer probe: full-size parity of library variants against the reference.
 
 python tools/variant_parity.py c5 [c3 c2 ...]  — for each config, the reference's csfmm_sum
-(oracle/_ref, host cores) is computed once and cached under gpurun_out/; then every
+(oracle/_ref, host cores) is computed once and cached under /tmp; then every
 _variants/*/libcsfs_b200.so (and the in-tree library) is run in a subprocess
 (CSFS_B200_LIB) and its relative L2 against the reference printed (one JSON line per
 variant and config)."""
@@ -38,7 +38,7 @@ def main():
     os.makedirs("gpurun_out", exist_ok=True)
     libs = sorted(glob.glob("_variants/*/libcsfs_b200.so")) + ["paper_2508_13550_b200/libcsfs_b200.so"]
     for name in sys.argv[1:]:
-        cache = f"gpurun_out/ref_{name}.npy"
+        cache = f"/tmp/ref_{name}.npy"
         if not os.path.exists(cache):
             wl = configs.make(name)
             r, _ = ref.csfmm(wl.xyz, wl.xyz, wl.weights, wl.kernel, mac=wl.mac, degree=wl.degree, n0=wl.n0)
