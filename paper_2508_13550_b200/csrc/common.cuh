@@ -23,7 +23,7 @@ constexpr double kCoincidenceTol = 1e-14;  // kernels.hpp:28
 constexpr double kNodeTol = 1e-14;         // interpolation.cpp:8
 constexpr int kMaxDepth = 60;              // cluster_tree.cpp:11
 constexpr double kMinExtent = 1e-13;       // cluster_tree.cpp:12
-constexpr int kLogTabBits = 11;            // fastmath.cuh log table: 2048 mantissa intervals
+constexpr int kLogTabBits = 12;            // fastmath.cuh log table: 4096 mantissa intervals
 constexpr int kLogTab = 1 << kLogTabBits;
 constexpr int kLogTabWords = kLogTab;      // double2 words of the global table
 

@@ -3,17 +3,20 @@
 // The evaluation phases are FP64-issue bound.  libdevice's log is
 // ~28 FP64 instructions, sqrt and a/b ~8 each; the kernel functors need:
 //   log   -> Tang-style table method with an accurate table (Gal): x = 2^k m with
-//            m in [0.7070, 1.4141) (so both sides of x = 1 have k = 0), m r_i = 1 + t,
-//            |t| <= 2^-11, from a 2048-entry table of {r_i, L_i} (32 KB, dynamic shared
-//            memory): r_i is chosen near 1/centre_i so that L_i = -ln r_i is within 2^-67
-//            of the 2^-46 grid (tools/gen_log_table.c): one LDS.128 per lookup.  The two
-//            intervals around 1 use r = 1, L = 0, so t = m - 1 is exact — branch-free.
-//            k ln2 + L_i in one FMA, log1p(t) by a degree-4 polynomial: 7 FP64
-//            instructions (+ one int->double conversion).  Error <= 1 ulp + |t|^5/5
-//            (<= 5.6e-18 absolute, reached only in the interval just above 1, where the value
-//            is ~t: up to ~100 ulp RELATIVE there); the kernels add log to O(1) terms, so
-//            only the absolute error reaches them (tests/test_gpu_numerics.py).  Domain:
-//            positive normals.
+//            m in [0.7070, 1.4141), m r_i / LAM = 1 + t, |t| <= 2^-13, from a 4096-entry
+//            table of {r_i, L_i} (64 KB, dynamic shared memory; tools/gen_log_table.c):
+//            r_i is stored scaled by LAM = fl(1/sqrt(3)) and chosen so that
+//            L_i = -ln(r_i / LAM) is within 2^-67 of the 2^-46 grid: one LDS.128 per lookup.
+//            t' = fma(m, r_i, -LAM) = LAM t (one rounding at |t'| < 2^-13), and with
+//            LAM^2 = 1/3 the degree-3 log1p t + c2 t^2 + t^3/3 becomes
+//            (t' + t'^2 (t' + c2/LAM)) / LAM: a DADD and two DFMA whose constants all sit in
+//            uniform registers (no per-pair materialised constant), k ln2 + L_i in one FMA:
+//            6 FP64 instructions (+ one int->double conversion).  c2 = -1/2 - (sqrt2-1)/2 h^2
+//            (h = 2^-13) balances the truncated t^4/4 term: |error| <= 0.043 h^4 = 9.5e-18
+//            ABSOLUTE + rounding (~1 ulp) — what the kernels consume: every log is added to
+//            O(1) terms or multiplied by an O(10) factor (tests/test_gpu_numerics.py).  m = 1
+//            sits mid-interval ([1 - 2^-14, 1 + 2^-13), r = LAM, L = 0): log(1) = 0 exactly
+//            (t = m - 1 exact up to the LAM scaling).  Domain: positive normals.
 //   rsqrt -> MUFU.RSQ64H seed + one cubic-convergent correction (5 FP64), <= 2 ulp.
 //   rcp   -> MUFU.RCP64H seed + one cubic-convergent correction (3 FP64), <= 2 ulp.
 // Arguments are finite positive normals (the coincidence guard keeps 1 - x.y >= 1e-14).
@@ -37,8 +40,11 @@ __device__ __forceinline__ LogTable stage_log_table(double2* sm, const double2* 
     return LogTable{sm};
 }
 
-constexpr int kLogOff = 0x3fe6a000;              // high word of the lowest m (~0.70703)
+constexpr int kLogOff = 0x3fe6a080;  // high word of the lowest m (~0.7071); m = 1 mid-interval
 constexpr double kLn2 = 0x1.62e42fefa39efp-1;
+constexpr double kLogLam = 0x1.279a74590331cp-1;    // fl(1/sqrt(3)): the table's r_i scale
+constexpr double kLogMu = 0x1.bb67ae8584cabp+0;     // fl(1/kLogLam)
+constexpr double kLogKappa = -0x1.bb67aeb36f4fbp-1; // c2 / kLogLam, c2 = -1/2 - (sqrt2-1)/2 2^-26
 
 __device__ __forceinline__ double fast_log(double x, const LogTable& tb) {
     const int hi = __double2hiint(x);
@@ -47,12 +53,11 @@ __device__ __forceinline__ double fast_log(double x, const LogTable& tb) {
     const int i = (d >> (20 - kLogTabBits)) & (kLogTab - 1);
     const double m = __hiloint2double(hi - (k << 20), __double2loint(x));
     const double2 e = tb.e[i];
-    // |t| <= 2^-11; exact for the two intervals around m = 1 (r = 1)
-    const double t = fma(m, e.x, -1.0);
-    const double p = fma(fma(-1.0 / 4.0, t, 1.0 / 3.0), t, -1.0 / 2.0);
+    const double tp = fma(m, e.x, -kLogLam);        // LAM t, |t| <= 2^-13
+    const double q = fma(tp * tp, tp + kLogKappa, tp);  // LAM log1p(t)
     // k ln2 + L_i in one FMA (k ln2 rounded once inside it; |k| <= 1 for most arguments)
     const double A = fma(double(k), kLn2, e.y);
-    return A + fma(t * t, p, t);
+    return fma(q, kLogMu, A);
 }
 
 __device__ __forceinline__ double rsqrt_seed(double x) {

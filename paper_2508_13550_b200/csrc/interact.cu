@@ -631,6 +631,7 @@ void eval_pairs(const KernelSpec& k, const double* x, const double* y, long long
                 const double2* log_tab, cudaStream_t s) {
     if (n == 0) return;
     with_op(k, [&](auto op) {
+        allow_table_smem(k_eval_pairs<decltype(op)>);
         k_eval_pairs<<<ceil_div(n, 128), 128, kLogTabBytes, s>>>(op, x, y, n, out, log_tab);
         CSFS_LAUNCH_CHECK();
     });
@@ -638,6 +639,7 @@ void eval_pairs(const KernelSpec& k, const double* x, const double* y, long long
 
 void eval_math(int fn, const double* x, long long n, double* out, const double2* log_tab, cudaStream_t s) {
     if (n == 0) return;
+    allow_table_smem(k_eval_math);
     k_eval_math<<<ceil_div(n, 128), 128, kLogTabBytes, s>>>(fn, x, n, out, log_tab);
     CSFS_LAUNCH_CHECK();
 }

@@ -98,9 +98,10 @@ def test_configs_deterministic_and_shaped():
 
 
 def test_log_table():
-    """fastmath.cuh's accurate log table (tools/gen_log_table.c): 2048 intervals of m in
-    [hi 0x3fe6a000, +2^20), r = 1 and L = 0 on the two intervals around m = 1, elsewhere
-    L_i on the 2^-46 grid within 2^-67 of -ln r_i, and |m r_i - 1| <= 2^-11 on every interval."""
+    """fastmath.cuh's accurate log table (tools/gen_log_table.c): 4096 intervals of m in
+    [hi 0x3fe6a080, +2^20), r_i stored scaled by LAM = fl(1/sqrt 3); the interval holding
+    m = 1 (mid-interval) is {LAM, 0}, elsewhere L_i on the 2^-46 grid within 2^-67 of
+    -ln(r_i / LAM); |m r_i / LAM - 1| <= 2^-13 on every interval."""
     import struct
     from fractions import Fraction
 
@@ -108,23 +109,25 @@ def test_log_table():
     mpmath.mp.prec = 160
     src = open(os.path.join(ROOT, "paper_2508_13550_b200", "csrc", "log_table.inc")).read()
     ents = re.findall(r"\{(-?0x[0-9a-fp.+\-]+), (-?0x[0-9a-fp.+\-]+)\}", src)
-    n = 2048
-    w = 20 - 11
+    n, bits = 4096, 12
+    w = 20 - bits
     assert len(ents) == n
-    one = (0x3FF00000 - 0x3FE6A000) >> w
+    lam = float.fromhex("0x1.279a74590331cp-1")
+    assert lam == float(1 / mpmath.sqrt(3))
 
     def from_hi(h):
         return struct.unpack(">d", struct.pack(">Q", h << 32))[0]
 
     for i, (a, b) in enumerate(ents):
         r, L = float.fromhex(a), float.fromhex(b)
-        lo, hi = from_hi(0x3FE6A000 + (i << w)), from_hi(0x3FE6A000 + ((i + 1) << w))
-        if i in (one - 1, one):
-            assert (r, L) == (1.0, 0.0) and lo <= 1.0 <= hi
+        lo, hi = from_hi(0x3FE6A080 + (i << w)), from_hi(0x3FE6A080 + ((i + 1) << w))
+        if lo <= 1.0 < hi:
+            assert (r, L) == (lam, 0.0)
             continue
         assert (Fraction(L) * 2 ** 46).denominator == 1
-        assert abs(-mpmath.log(mpmath.mpf(r)) - mpmath.mpf(L)) < mpmath.mpf(2) ** -67
-        assert max(abs(Fraction(lo) * Fraction(r) - 1), abs(Fraction(hi) * Fraction(r) - 1)) <= Fraction(1, 2048)
+        assert abs(-mpmath.log(mpmath.mpf(r) / mpmath.mpf(lam)) - mpmath.mpf(L)) < mpmath.mpf(2) ** -67
+        rl = Fraction(r) / Fraction(lam)
+        assert max(abs(Fraction(lo) * rl - 1), abs(Fraction(hi) * rl - 1)) <= Fraction(1, 8192) * (1 + Fraction(1, 1024))
 
 
 def test_bve_mirror_defaults_and_sequencing():
