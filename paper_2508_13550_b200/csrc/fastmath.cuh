@@ -51,7 +51,11 @@ __device__ __forceinline__ double fast_log(double x, const LogTable& tb) {
     const int d = hi - kLogOff;
     const int k = d >> 20;  // arithmetic shift: x = 2^k m, m in [0.7070, 1.4141)
     const int i = (d >> (20 - kLogTabBits)) & (kLogTab - 1);
-    const double m = __hiloint2double(hi - (k << 20), __double2loint(x));
+    // hi - k 2^20 as ONE integer multiply-add (written as k << 20 the compiler forms
+    // d & 0xfff00000 and a subtraction: two instructions per log)
+    int mhi;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(mhi) : "r"(k), "n"(-1048576), "r"(hi));
+    const double m = __hiloint2double(mhi, __double2loint(x));
     const double2 e = tb.e[i];
     const double tp = fma(m, e.x, -kLogLam);        // LAM t, |t| <= 2^-13
     const double q = fma(tp * tp, tp + kLogKappa, tp);  // LAM log1p(t)

@@ -259,11 +259,12 @@ struct MutualParams {
     long long own_b, own_e;
 };
 
-// double butterfly shuffle as two explicit 32-bit halves (keeps the halves in place; the
+// double butterfly shuffle as two explicit 32-bit halves in one asm block (keeps the halves in place; the
 // generic double overload let ptxas swap them and re-pair with moves)
 __device__ __forceinline__ double shfl_xor_d(double v, int m) {
-    const int lo = __shfl_xor_sync(0xffffffffu, __double2loint(v), m);
-    const int hi = __shfl_xor_sync(0xffffffffu, __double2hiint(v), m);
+    int lo, hi;
+    asm volatile("shfl.sync.bfly.b32 %0, %2, %4, 0x1f, -1;\n\tshfl.sync.bfly.b32 %1, %3, %4, 0x1f, -1;"
+                 : "=r"(lo), "=r"(hi) : "r"(__double2loint(v)), "r"(__double2hiint(v)), "r"(m));
     return __hiloint2double(hi, lo);
 }
 
