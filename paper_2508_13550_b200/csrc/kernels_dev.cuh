@@ -10,7 +10,7 @@
 //    and the weight zeroed) instead of branched: no divergence, exact skip semantics; the
 //    compare itself runs on the integer pipe (not_coincident, common.cuh);
 //  * the prefactor (-1/4pi, 1/4pi, 3 rho/4pi) is applied once per target (`scale`);
-//  * log / rsqrt / rcp come from fastmath.cuh (11 / 5 / 3 FP64 instructions instead of
+//  * log / rsqrt / rcp come from fastmath.cuh (6 / 5 / 3 FP64 instructions instead of
 //    libdevice's ~28 / 8+8 / 8), each within a few ulp;
 //  * SAL: targets enter halved, so 0.5 - t'.s = omc/2 exactly; 2/gamma = rsqrt(omc/2),
 //    s = gamma/2 = (omc/2) rsqrt(omc/2), log(s (1 + s)) = log(fma(s, s, s)) — the
