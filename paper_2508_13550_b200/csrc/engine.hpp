@@ -118,6 +118,7 @@ struct Lists {
     DevBuf<int2> l[4];  // pp, pc, cp, cc
     long long n[4] = {0, 0, 0, 0};
     DevBuf<int2> front, front2;
+    DevBuf<int> cnt;  // sweep counters of the host-free traversal
 };
 
 // Work items for the unified evaluation kernel: one item per target leaf (PP+PC

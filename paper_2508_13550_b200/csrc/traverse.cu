@@ -272,6 +272,68 @@ __global__ void k_mutual_sort(int ncl, const int* __restrict__ mcnt, const int* 
     warp_sort_unique(mlist + moff[X], mcnt[X], lane);
 }
 
+// One sweep of the dual traversal without a host round trip: every frontier pair is
+// classified (classify = the reference's decision, summation.cpp:177-200); list entries and
+// the split pairs' children are appended with warp-aggregated atomics (one atomic per warp
+// and category).  The order of the entries is therefore arbitrary, but nothing depends on
+// it: build_items sorts every work item's entries by (type, source) — the reference's
+// accumulation order — and the lists are compared as sets.  Counters that pass a buffer's
+// capacity raise *overflow (the caller then re-runs the synchronous sweep loop).
+__global__ void __launch_bounds__(256) k_traverse_step(const TreeView T, const TreeView S, double mac, int n0,
+                                                       const int2* __restrict__ fin, const int* __restrict__ fcnt,
+                                                       int2* fout, int* fcnt_next, long long fcap, int2* l0, int2* l1,
+                                                       int2* l2, int2* l3, int* lcnt, long long lcap, int* overflow) {
+    const int F = *fcnt;
+    const int lane = threadIdx.x & 31;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < F; base += stride) {
+        const long long i = base + lane;
+        int cat = -1;
+        int2 p = make_int2(0, 0);
+        if (i < F) {
+            p = fin[i];
+            cat = classify(T, S, p.x, p.y, mac, n0);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, cat == k);
+            if (m == 0u) continue;
+            const int leader = __ffs(m) - 1;
+            int at = 0;
+            if (lane == leader) at = atomicAdd(&lcnt[k], __popc(m));
+            at = __shfl_sync(0xffffffffu, at, leader);
+            if (cat == k) {
+                const long long pos = (long long)at + __popc(m & ((1u << lane) - 1u));
+                int2* l = k == 0 ? l0 : k == 1 ? l1 : k == 2 ? l2 : l3;
+                if (pos < lcap) l[pos] = p;
+                else *overflow = 1;
+            }
+        }
+        const int nc = cat == 4 ? S.nchild[p.y] : cat == 5 ? T.nchild[p.x] : 0;
+        int incl = nc;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot == 0) continue;
+        int at = 0;
+        if (lane == 31) at = atomicAdd(fcnt_next, tot);
+        at = __shfl_sync(0xffffffffu, at, 31);
+        if (nc) {
+            const long long pos = (long long)at + incl - nc;
+            if (pos + nc > fcap) {
+                *overflow = 1;
+            } else {
+                const int4 ch = cat == 4 ? S.child[p.y] : T.child[p.x];
+                const int cs[4] = {ch.x, ch.y, ch.z, ch.w};
+                for (int q = 0; q < nc; ++q) fout[pos + q] = cat == 4 ? make_int2(p.x, cs[q]) : make_int2(cs[q], p.y);
+            }
+        }
+    }
+}
+
 }  // namespace
 
 void partition_units(const DeviceTree& t, std::vector<long long>& ub, std::vector<long long>& ue) {
@@ -384,6 +446,48 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
     CSFS_LAUNCH_CHECK();
 }
 
+// The sweeps without host round trips: a pair (t, s) of the frontier at sweep k has
+// depth(t) + depth(s) = k (every split deepens one side), so depth_t + depth_s + 1 sweeps
+// drain it; all of them are enqueued at once and the counts are read back once.  Buffers
+// are sized from their current capacity (grown by earlier calls) or a first guess; if a
+// sweep overflows one, the caller falls back to the synchronous loop, which grows them.
+static bool dual_traversal_async(const TreeView& T, const TreeView& S, int depth_sum, double mac, int n0,
+                                 const std::vector<int2>& seeds, long long guess, Lists& L, Scratch& sc,
+                                 cudaStream_t s) {
+    const int K = depth_sum + 1;
+    long long lcap = guess;
+    for (int k = 0; k < 4; ++k) lcap = std::max<long long>(lcap, (long long)L.l[k].cap);
+    for (int k = 0; k < 4; ++k) L.l[k].grow(size_t(lcap));
+    for (int k = 0; k < 4; ++k) lcap = std::min<long long>(lcap, (long long)L.l[k].cap);
+    long long fcap = std::max<long long>(2 * guess, (long long)std::max(L.front.cap, L.front2.cap));
+    L.front.grow(size_t(fcap));
+    L.front2.grow(size_t(fcap));
+    fcap = std::min<long long>((long long)L.front.cap, (long long)L.front2.cap);
+    L.cnt.grow(size_t(K + 8));
+    int* fc = L.cnt.p;            // [0, K]: frontier sizes per sweep
+    int* lc = L.cnt.p + K + 1;    // 4 list counts
+    int* ovf = L.cnt.p + K + 5;   // overflow flag
+    CSFS_CK(cudaMemsetAsync(L.cnt.p, 0, (K + 8) * sizeof(int), s));
+    sc.host[32] = int(seeds.size());
+    CSFS_CK(cudaMemcpyAsync(fc, sc.host + 32, sizeof(int), cudaMemcpyHostToDevice, s));
+    CSFS_CK(cudaMemcpyAsync(L.front.p, seeds.data(), seeds.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    int dev = 0, sms = 0;
+    CSFS_CK(cudaGetDevice(&dev));
+    CSFS_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    for (int k = 0; k < K; ++k) {
+        const int2* fin = (k & 1) ? L.front2.p : L.front.p;
+        int2* fout = (k & 1) ? L.front.p : L.front2.p;
+        k_traverse_step<<<4 * sms, 256, 0, s>>>(T, S, mac, n0, fin, fc + k, fout, fc + k + 1, fcap, L.l[0], L.l[1],
+                                                L.l[2], L.l[3], lc, lcap, ovf);
+        CSFS_LAUNCH_CHECK();
+    }
+    CSFS_CK(cudaMemcpyAsync(sc.host, fc + K, 6 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaStreamSynchronize(s));
+    if (sc.host[5] != 0 || sc.host[0] != 0) return false;  // overflow, or pairs left (cannot happen)
+    for (int k = 0; k < 4; ++k) L.n[k] = sc.host[1 + k];
+    return true;
+}
+
 void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, int n0, Lists& L,
                     Scratch& sc, cudaStream_t s) {
     const TreeView T = tgt.view(), S = src.view();
@@ -391,6 +495,11 @@ void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, in
     for (int t = 0; t < 6; ++t)
         for (int q = 0; q < 6; ++q)
             if (tgt.root_count[t] > 0 && src.root_count[q] > 0) seeds.push_back(make_int2(t, q));
+    for (int k = 0; k < 4; ++k) L.n[k] = 0;
+    if (seeds.empty()) return;
+    if (dual_traversal_async(T, S, tgt.depth_max() + src.depth_max(), mac, n0, seeds,
+                             16LL * (tgt.ncl + src.ncl) + 4096, L, sc, s))
+        return;
     for (int k = 0; k < 4; ++k) L.n[k] = 0;
     long long F = (long long)seeds.size();
     L.front.grow(std::max<long long>(F, 64));
