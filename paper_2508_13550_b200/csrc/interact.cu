@@ -80,6 +80,12 @@ struct InteractParams {
     const int* anchor;  // per item owner key (nullptr: every item is ours)
     long long own_b, own_e;
     const double2* log_tab;  // kLogTabWords entries (fastmath.cuh)
+    // symmetric-pair partial blocks of each item's key (k_mutual ran first), added to the
+    // item's outputs in ascending block order; mcnt == nullptr: none
+    const int* keys;
+    const int *mcnt, *moff;
+    const long long* mlist;
+    const double* partial;
 };
 
 template <class Op>
@@ -226,11 +232,25 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
             }
             if (g == 0) {
                 const double sc = op.scale();
+                int mn = 0;
+                const long long* ml = nullptr;
+                if constexpr (D == 1) {
+                    if (P.mcnt) {
+                        const int X = P.keys[it];
+                        mn = P.mcnt[X];
+                        ml = P.mlist + P.moff[X];
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < kTPT; ++k)
                     if (act[k])
 #pragma unroll
-                        for (int c = 0; c < D; ++c) OUT[(long long)(d.x + t0 + r + k * gs) * D + c] = acc[k][c] * sc;
+                        for (int c = 0; c < D; ++c) {
+                            const int x = t0 + r + k * gs;
+                            double v = acc[k][c] * sc;
+                            for (int a = 0; a < mn; ++a) v += P.partial[ml[a] + x];  // D == 1
+                            OUT[(long long)(d.x + x) * D + c] = v;
+                        }
             }
         }
     }
@@ -245,7 +265,8 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
 // are reduced per warp with a select-free transposed butterfly (4+2+1+1+1 shuffles per 8
 // sources, each lane visiting the batch in its own XOR order), then over the group's warps
 // in fixed order: deterministic, no atomics.  Both partial sums go
-// to `partial`; k_mutual_reduce adds them to phi_near after the list items.
+// to `partial`; k_interact, which runs after it, adds every block of a work item's key to
+// the item's outputs in ascending block order.
 struct MutualParams {
     const int4* pair;       // {A begin, |A|, B begin, |B|}, |A|, |B| <= 256; negative: proxy sets (CC)
     const long long* poff;  // partial offset of A's block (B's follows at + |A|)
@@ -403,30 +424,6 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
     }
 }
 
-// phi_near[x] (leaf keys X < ncl) or qphi[c*npp + m] (cluster keys X = ncl + c) += every
-// symmetric-pair partial of that point set, in ascending partial order.  One CTA per key;
-// owned sets only.
-__global__ void k_mutual_reduce(int ncl, int npp, const int* __restrict__ begin, const int* __restrict__ end,
-                                const int* __restrict__ mcnt, const int* __restrict__ moff,
-                                const long long* __restrict__ mlist, const double* __restrict__ partial,
-                                double* phi, double* qphi, long long own_b, long long own_e) {
-    const int X = blockIdx.x;
-    const int n = mcnt[X];
-    if (n == 0) return;
-    const bool leaf = X < ncl;
-    const int c = leaf ? X : X - ncl;
-    const int b = begin[c];
-    if (b < own_b || b >= own_e) return;
-    double* out = leaf ? phi + b : qphi + (long long)c * npp;
-    const int len = leaf ? end[c] - b : npp;
-    const long long* l = mlist + moff[X];
-    for (int x = threadIdx.x; x < len; x += blockDim.x) {
-        double v = out[x];
-        for (int a = 0; a < n; ++a) v += partial[l[a] + x];
-        out[x] = v;
-    }
-}
-
 __global__ void k_aos_to_soa(const double* __restrict__ xyz, long long n, double* x, double* y, double* z) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -570,15 +567,17 @@ void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src,
         m.own_b = own.b;
         m.own_e = own.e;
     }
+    if (items.mutual) {  // k_interact adds the symmetric-pair blocks (after k_mutual, same stream)
+        p.keys = items.keys;
+        p.mcnt = items.mcnt;
+        p.moff = items.moff;
+        p.mlist = items.mlist;
+        p.partial = items.partial;
+    }
     with_op(k, [&](auto op) {
         if (items.mutual) launch_mutual(m, op, s);
         launch(p, op, s);
     });
-    if (items.mutual) {
-        k_mutual_reduce<<<2 * tgt.ncl, 128, 0, s>>>(tgt.ncl, tgt.npp, tgt.begin, tgt.end, items.mcnt, items.moff,
-                                                    items.mlist, items.partial, phi_near, tgt.qphi, own.b, own.e);
-        CSFS_LAUNCH_CHECK();
-    }
 }
 
 void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, const double* sxyz,
