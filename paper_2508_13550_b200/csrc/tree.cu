@@ -564,15 +564,18 @@ __global__ void k_proxy(int ncl, int np, Cheb cheb, const int* __restrict__ face
 __global__ void k_qrad(int ncl, int npp, const double* __restrict__ cx, const double* __restrict__ cy,
                        const double* __restrict__ cz, const double* __restrict__ qx, const double* __restrict__ qy,
                        const double* __restrict__ qz, double* qrad) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncl) return;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;  // a warp per cluster
+    if (c >= ncl) return;  // warp-uniform
+    const double ox = cx[c], oy = cy[c], oz = cz[c];
     double r2 = 0.0;
-    for (int k = 0; k < npp; ++k) {
+    for (int k = lane; k < npp; k += 32) {  // consecutive proxies: coalesced
         const long long g = (long long)c * npp + k;
-        const double dx = qx[g] - cx[c], dy = qy[g] - cy[c], dz = qz[g] - cz[c];
+        const double dx = qx[g] - ox, dy = qy[g] - oy, dz = qz[g] - oz;
         r2 = fmax(r2, dx * dx + dy * dy + dz * dz);
     }
-    qrad[c] = sqrt(r2);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, d));  // max: order-free
+    if (lane == 0) qrad[c] = sqrt(r2);
 }
 
 __global__ void k_gather(long long n, const int* __restrict__ perm, const double* __restrict__ src,
@@ -885,7 +888,8 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
                                                           t.eta0, t.eta1, t.qx, t.qy, t.qz);
     CSFS_LAUNCH_CHECK();
     t.qrad.grow(std::max(t.ncl, 1));
-    k_qrad<<<ceil_div(t.ncl, kThreads), kThreads, 0, s>>>(t.ncl, t.npp, t.cx, t.cy, t.cz, t.qx, t.qy, t.qz, t.qrad);
+    k_qrad<<<ceil_div((long long)t.ncl * 32, kThreads), kThreads, 0, s>>>(t.ncl, t.npp, t.cx, t.cy, t.cz, t.qx, t.qy,
+                                                                          t.qz, t.qrad);
     CSFS_LAUNCH_CHECK();
 }
 
