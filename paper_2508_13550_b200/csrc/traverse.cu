@@ -10,6 +10,8 @@
 // (list type, source id) order so results are deterministic run to run.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "engine.hpp"
 #include "scan.cuh"
 
@@ -283,7 +285,8 @@ __global__ void __launch_bounds__(256) k_traverse_step(const TreeView T, const T
                                                        const int2* __restrict__ fin, const int* __restrict__ fcnt,
                                                        int2* fout, int* fcnt_next, long long fcap, int2* l0, int2* l1,
                                                        int2* l2, int2* l3, int* lcnt, long long lcap, int* overflow) {
-    const int F = *fcnt;
+    // after an overflow the counts no longer describe the buffers: drain (the caller re-runs)
+    const int F = *overflow ? 0 : int(min((long long)*fcnt, fcap));
     const int lane = threadIdx.x & 31;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < F; base += stride) {
@@ -497,9 +500,14 @@ void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, in
             if (tgt.root_count[t] > 0 && src.root_count[q] > 0) seeds.push_back(make_int2(t, q));
     for (int k = 0; k < 4; ++k) L.n[k] = 0;
     if (seeds.empty()) return;
-    if (dual_traversal_async(T, S, tgt.depth_max() + src.depth_max(), mac, n0, seeds,
-                             16LL * (tgt.ncl + src.ncl) + 4096, L, sc, s))
-        return;
+    // first-guess buffer size; CSFS_B200_TRAVERSAL_GUESS overrides it (the tests force the
+    // overflow fallback with a tiny one)
+    static const long long guess_env = [] {
+        const char* e = std::getenv("CSFS_B200_TRAVERSAL_GUESS");
+        return e ? std::atoll(e) : 0LL;
+    }();
+    const long long guess = guess_env > 0 ? guess_env : 16LL * (tgt.ncl + src.ncl) + 4096;
+    if (dual_traversal_async(T, S, tgt.depth_max() + src.depth_max(), mac, n0, seeds, guess, L, sc, s)) return;
     for (int k = 0; k < 4; ++k) L.n[k] = 0;
     long long F = (long long)seeds.size();
     L.front.grow(std::max<long long>(F, 64));

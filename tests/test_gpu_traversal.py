@@ -1,0 +1,62 @@
+"""GPU: the two paths of the dual traversal (traverse.cu).  The host-free sweeps (all
+depth_t + depth_s + 1 sweeps enqueued at once, warp-aggregated atomic appends) run from
+the buffers' current capacity; when a sweep would overflow one, the synchronous scan loop
+runs instead and grows them.  A tiny first guess (CSFS_B200_TRAVERSAL_GUESS) forces the
+fallback on the first call; the second call on the same context takes the host-free path
+with the grown buffers.  Both must give the reference's lists (as sets) and the same
+potentials bit for bit (every work item's entries are sorted by (type, source), so the
+sweep order cannot reach the sums)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import ref
+from paper_2508_13550_b200 import Engine, Kernel, ParticleSet, TraversalConfig
+from paper_2508_13550_b200.grids import cubed_sphere
+
+def sorted_pairs(a):
+    a = np.asarray(a).reshape(-1, 2)
+    return a[np.lexsort((a[:, 1], a[:, 0]))] if a.size else a
+
+xyz, area = cubed_sphere(6)
+w = xyz[:, 0] * xyz[:, 1] * xyz[:, 2] * area
+eng = Engine(0)
+cfg = TraversalConfig(mac=0.6, degree=6, n0=32)
+rt = ref.Tree(xyz, 6, 32)
+rl = ref.lists(rt, rt, 0.6, 32)
+out, same_lists = [], []
+for call in range(2):
+    g = eng.csfmm_sum(ParticleSet(xyz, w), ParticleSet(xyz, w), Kernel.parse("sal"), cfg).values
+    gl = eng.lists_export()
+    same_lists.append(all(np.array_equal(gl[k], sorted_pairs(rl[k])) for k in ("pp", "pc", "cp", "cc")))
+    out.append(g)
+r, _ = ref.csfmm(xyz, xyz, w, "sal", mac=0.6, degree=6, n0=32)
+print(json.dumps({"lists": same_lists, "bitwise": bool(np.array_equal(out[0], out[1])),
+                  "rel_l2": float(np.sqrt(np.sum((out[1] - r) ** 2) / np.sum(r ** 2))),
+                  "n_pp": int(len(rl["pp"]))}))
+"""
+
+
+@pytest.mark.parametrize("guess", ["64", "0"])
+def test_traversal_paths(guess):
+    env = dict(os.environ)
+    if guess != "0":
+        env["CSFS_B200_TRAVERSAL_GUESS"] = guess  # 64 entries: the first call must overflow
+    res = subprocess.run([sys.executable, "-c", CHILD, ROOT], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    d = json.loads(res.stdout.strip().splitlines()[-1])
+    assert d["n_pp"] > 64
+    assert d["lists"] == [True, True]
+    assert d["bitwise"]
+    assert d["rel_l2"] < 1e-10
