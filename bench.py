@@ -11,7 +11,10 @@ PP/PC/CP/CC + downward, output in input order.
          ranks (N > 1: target-partitioned, NCCL all-reduce of proxy weights + potentials)
   e2e    the same through the host-pointer C-ABI (csfs_b200_csfmm): pinned host inputs
          copied H2D and the result copied D2H inside every step
-  roofline  the evaluation kernel (k_interact) against the MEASURED FP64 DFMA peak
+  roofline  the evaluation phase (k_mutual + k_interact, 95% of the step) against the
+         MEASURED FP64 DFMA peak: `achieved` by SURVEY.md §8d's per-pair convention (87
+         flop for SAL, so frac > 1 — the functor executes ~34), `executed_frac` from the
+         ncu-measured FP64 flop per pair (profiles/*interact_sal_ncu.json)
   cpu_baseline  the reference's own csfmm_sum (oracle/_ref, all host cores) on a bounded
          sample of the same workload (one depth-1 face quadrant of targets, all sources)
 
