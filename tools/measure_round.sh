@@ -13,4 +13,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"^k_mutual$" -c 1 -o gpurun_out/prof_${T}_mut python tools/prof_once.py c5 > gpurun_out/ncu_mut_$T.log 2>&1
 timeout 1800 ncu --set full --clock-control none --import-source on --replay-mode application -k regex:"^k_interact$" -c 1 -o gpurun_out/prof_${T}_int python tools/prof_once.py c5 > gpurun_out/ncu_int_$T.log 2>&1
 for r in mut int; do ncu -i gpurun_out/prof_${T}_$r.ncu-rep --page raw --csv > gpurun_out/prof_${T}_$r.csv 2>/dev/null; done
+python tools/ncu_eval_summary.py $T > gpurun_out/ncu_eval_summary_$T.log 2>&1
 echo done
