@@ -18,17 +18,17 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-template <int K, int THREADS = kScanThreads>
-__device__ __forceinline__ void block_exclusive_scan(int (&v)[K], int (&total)[K]) {
-    __shared__ int warp_tot[THREADS / 32][K];
+template <int K, int THREADS = kScanThreads, class T = int>
+__device__ __forceinline__ void block_exclusive_scan(T (&v)[K], T (&total)[K]) {
+    __shared__ T warp_tot[THREADS / 32][K];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int incl[K];
+    T incl[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        int x = v[k];
+        T x = v[k];
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, d);
+            const T y = __shfl_up_sync(0xffffffffu, x, d);
             if (lane >= d) x += y;
         }
         incl[k] = x;
@@ -39,9 +39,9 @@ __device__ __forceinline__ void block_exclusive_scan(int (&v)[K], int (&total)[K
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        int pre = 0, tot = 0;
+        T pre = 0, tot = 0;
         for (int w = 0; w < THREADS / 32; ++w) {
-            const int t = warp_tot[w][k];
+            const T t = warp_tot[w][k];
             if (w < warp) pre += t;
             tot += t;
         }
@@ -51,18 +51,19 @@ __device__ __forceinline__ void block_exclusive_scan(int (&v)[K], int (&total)[K
     __syncthreads();
 }
 
-// f(i, int c[K]) writes the K counts of element i (c is zeroed before the call).
-template <int K, class F>
-__global__ void __launch_bounds__(kScanThreads) scan_tile_totals(long long n, F f, int* tile_tot) {
+// f(i, T c[K]) writes the K counts of element i (c is zeroed before the call).  T is the
+// counter type: int, or long long where a total can pass INT_MAX (partial-sum offsets).
+template <int K, class T, class F>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_totals(long long n, F f, T* tile_tot) {
     const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-    int t[K];
+    T t[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) t[k] = 0;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
         const long long i = base + j;
         if (i < n) {
-            int c[K];
+            T c[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) c[k] = 0;
             f(i, c);
@@ -70,8 +71,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_totals(long long n, F 
             for (int k = 0; k < K; ++k) t[k] += c[k];
         }
     }
-    int tot[K];
-    block_exclusive_scan<K>(t, tot);
+    T tot[K];
+    block_exclusive_scan<K, kScanThreads, T>(t, tot);
     if (threadIdx.x == 0)
 #pragma unroll
         for (int k = 0; k < K; ++k) tile_tot[(long long)blockIdx.x * K + k] = tot[k];
@@ -82,15 +83,15 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_totals(long long n, F 
 constexpr int kTileScanThreads = 256;
 constexpr int kTileScanItems = 4;
 
-template <int K>
-__global__ void __launch_bounds__(kTileScanThreads) scan_tiles(int ntiles, int* tile_tot, int* grand) {
-    int carry[K];
+template <int K, class T>
+__global__ void __launch_bounds__(kTileScanThreads) scan_tiles(int ntiles, T* tile_tot, T* grand) {
+    T carry[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) carry[k] = 0;
     constexpr int kPass = kTileScanThreads * kTileScanItems;
     for (int b0 = 0; b0 < ntiles; b0 += kPass) {
         const int b = b0 + threadIdx.x * kTileScanItems;
-        int v[kTileScanItems][K], t[K];
+        T v[kTileScanItems][K], t[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) t[k] = 0;
 #pragma unroll
@@ -100,8 +101,8 @@ __global__ void __launch_bounds__(kTileScanThreads) scan_tiles(int ntiles, int* 
                 v[j][k] = (b + j < ntiles) ? tile_tot[(long long)(b + j) * K + k] : 0;
                 t[k] += v[j][k];
             }
-        int tot[K];
-        block_exclusive_scan<K, kTileScanThreads>(t, tot);
+        T tot[K];
+        block_exclusive_scan<K, kTileScanThreads, T>(t, tot);
 #pragma unroll
         for (int j = 0; j < kTileScanItems; ++j)
 #pragma unroll
@@ -117,13 +118,13 @@ __global__ void __launch_bounds__(kTileScanThreads) scan_tiles(int ntiles, int* 
         for (int k = 0; k < K; ++k) grand[k] = carry[k];
 }
 
-// e(i, const int c[K], const int pre[K]): pre = exclusive global prefix of each counter.
-template <int K, class F, class E>
+// e(i, const T c[K], const T pre[K]): pre = exclusive global prefix of each counter.
+template <int K, class T, class F, class E>
 __global__ void __launch_bounds__(kScanThreads)
-    scan_emit(long long n, F f, const int* tile_off, E e) {
+    scan_emit(long long n, F f, const T* tile_off, E e) {
     const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-    int c[kScanItems][K];
-    int t[K];
+    T c[kScanItems][K];
+    T t[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) t[k] = 0;
 #pragma unroll
@@ -135,9 +136,9 @@ __global__ void __launch_bounds__(kScanThreads)
 #pragma unroll
         for (int k = 0; k < K; ++k) t[k] += c[j][k];
     }
-    int tot[K];
-    block_exclusive_scan<K>(t, tot);
-    int pre[K];
+    T tot[K];
+    block_exclusive_scan<K, kScanThreads, T>(t, tot);
+    T pre[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) pre[k] = tile_off[(long long)blockIdx.x * K + k] + t[k];
 #pragma unroll
@@ -150,20 +151,26 @@ __global__ void __launch_bounds__(kScanThreads)
 }
 
 // Host driver: runs the three phases on `stream`.  `tile_buf` must hold
-// ceil(n/1024)*K ints, `grand` K ints (device).  Returns nothing; grand totals stay on
-// the device for the caller to fetch when it needs them.
-template <int K, class F, class E>
-void run_scan(long long n, F f, E e, int* tile_buf, int* grand, cudaStream_t stream) {
+// ceil(n/1024)*K counters, `grand` K counters (device).  Returns nothing; grand totals stay
+// on the device for the caller to fetch when it needs them.
+template <class T>
+struct NonDeduced {
+    using type = T;
+};
+
+template <int K, class T = int, class F, class E>
+void run_scan(long long n, F f, E e, typename NonDeduced<T>::type* tile_buf, typename NonDeduced<T>::type* grand,
+              cudaStream_t stream) {
     if (n <= 0) {
-        CSFS_CK(cudaMemsetAsync(grand, 0, K * sizeof(int), stream));
+        CSFS_CK(cudaMemsetAsync(grand, 0, K * sizeof(T), stream));
         return;
     }
     const int ntiles = ceil_div(n, kScanTile);
-    scan_tile_totals<K><<<ntiles, kScanThreads, 0, stream>>>(n, f, tile_buf);
+    scan_tile_totals<K, T><<<ntiles, kScanThreads, 0, stream>>>(n, f, tile_buf);
     CSFS_LAUNCH_CHECK();
-    scan_tiles<K><<<1, kTileScanThreads, 0, stream>>>(ntiles, tile_buf, grand);
+    scan_tiles<K, T><<<1, kTileScanThreads, 0, stream>>>(ntiles, tile_buf, grand);
     CSFS_LAUNCH_CHECK();
-    scan_emit<K><<<ntiles, kScanThreads, 0, stream>>>(n, f, tile_buf, e);
+    scan_emit<K, T><<<ntiles, kScanThreads, 0, stream>>>(n, f, tile_buf, e);
     CSFS_LAUNCH_CHECK();
 }
 
