@@ -5,14 +5,14 @@
  * (/root/reference/proj/include/csfs/summation.hpp).  Plain pointers and sizes only;
  * positions are AoS x,y,z doubles exactly as std::vector<csfs::Vec3>::data() lays them
  * out, weights/outputs are in INPUT order like the reference's ParticleSet /
- * PotentialField (summation.hpp:34-41).  The C++ shim (paper_2508_13550_b200/csrc/host/
- * csfs_b200.hpp) re-exposes the reference's csfs:: signatures on top of these entry
+ * PotentialField (summation.hpp:34-41).  The C++ shim (paper_2508_13550_b200/host/
+ * csfs_b200_shim.cpp) re-exposes the reference's csfs:: signatures on top of these entry
  * points and rethrows std::invalid_argument on code 1 with the reference's messages.
  *
  * Return codes: 0 ok, 1 invalid argument (reference's std::invalid_argument),
  * 2 CUDA error, 3 NCCL/collective error, 4 device out of memory.
- * One context per host thread; a context owns one device, one stream and its buffers;
- * calls on one context are serialized by the caller.
+ * One context per host thread; a context owns its device(s), streams, buffers and NCCL
+ * communicators; calls on one context are serialized by the caller.
  */
 #ifndef CSFS_B200_H
 #define CSFS_B200_H
@@ -68,9 +68,13 @@ typedef struct {
     int shared_tree;                             /* targets == sources: one tree built */
     uint64_t evals_executed;  /* kernel evaluations actually performed (symmetric PP/CC pairs once) */
     int symmetric_pairs;      /* PP leaf / CC cluster pairs evaluated once for both directions */
+    int n_ranks;              /* ranks that evaluated the call (1: one GPU) */
+    double t_exchange;        /* seconds in the two NCCL all-gathers (rank 0; 0 on one GPU) */
 } csfs_b200_stats;
 
 /* --- lifetime ------------------------------------------------------------------------ */
+/* One device.  (SURVEY.md §8b's csfs_b200_create(ctx, num_gpus, device_ids) is
+ * csfs_b200_create_multi below; this single-device form is its num_gpus = 1 case.) */
 CSFS_B200_API int csfs_b200_create(csfs_b200_ctx** out, int device);
 CSFS_B200_API void csfs_b200_destroy(csfs_b200_ctx* ctx);
 /* Message of the last failing call on this context ("" if none). */
@@ -155,7 +159,45 @@ CSFS_B200_API int csfs_b200_lists_export(csfs_b200_ctx* ctx, long long* counts, 
 /* Source-tree proxy weights after the upward pass, ncl x (p+1)^2, reference id order. */
 CSFS_B200_API int csfs_b200_proxy_weights_export(csfs_b200_ctx* ctx, double* pw);
 
-/* --- multi-GPU: target partitioning, one process per GPU ----------------------------------
+/* --- multi-GPU contexts: csfs_b200_csfmm / _csfmm_device / _bve_step on them run the
+ * target-partitioned CSFMM over every rank of the group, with the proxy-weight and
+ * potential exchanges as NCCL all-gathers over NVLink (partition.cu).  Results are bitwise
+ * identical for every rank count (and to the single-GPU engine up to the symmetric-pair
+ * scope: pairs never straddle two depth-1 subtrees, so they equal a one-GPU run with
+ * CSFS_B200_MUTUAL_SCOPE=unit bit for bit).  Other entry points run on rank 0's device.
+ * Calls on a group are collective: every rank of a Rank group makes the same call.
+ *
+ *   _create_multi     ONE process drives num_gpus devices (device_ids NULL = 0..num_gpus-1,
+ *                     distinct): ncclCommInitAll, one host thread + stream per device,
+ *                     rank 0 = device_ids[0] is the context's device; device pointers
+ *                     passed to it are on that device and the inputs are broadcast to
+ *                     the others over NVLink.
+ *   _create_rank      one process per GPU (e.g. torchrun): rank `rank` of `nranks`, NCCL
+ *                     from the CSFS_B200_NCCL_ID_BYTES unique id rank 0 made with
+ *                     csfs_b200_nccl_unique_id and shipped to the others; every rank passes
+ *                     the full inputs and receives the full result.
+ *   _create_emulated  nranks ranks on ONE device, run phase by phase with device copies in
+ *                     place of NCCL: the partition and exchange layout, bitwise, on one
+ *                     GPU (tests / per-rank cost measurement; not a speed-up).
+ * A failing NCCL call returns CSFS_B200_NCCL_ERROR (3). */
+#define CSFS_B200_NCCL_ID_BYTES 128
+CSFS_B200_API int csfs_b200_create_multi(csfs_b200_ctx** out, int num_gpus, const int* device_ids);
+CSFS_B200_API int csfs_b200_nccl_unique_id(unsigned char* id);
+CSFS_B200_API int csfs_b200_create_rank(csfs_b200_ctx** out, int device, int nranks, int rank,
+                                        const unsigned char* id);
+CSFS_B200_API int csfs_b200_create_emulated(csfs_b200_ctx** out, int device, int nranks);
+/* nranks / this rank / the devices of the group (nranks entries; Multi, Emulated: all,
+ * Rank: this process's) and, after a partitioned call, the owned tree-order target and
+ * source ranges of every rank (2 x nranks: begin, end).  Any pointer may be NULL. */
+CSFS_B200_API int csfs_b200_group_info(const csfs_b200_ctx* ctx, int* nranks, int* rank, int* devices,
+                                       long long* t_ranges, long long* s_ranges);
+
+/* TreeStats::leaf_size_histogram (cluster_tree.cpp:149-161) of the last call's target
+ * (which 0) or source (1) tree: bucket i counts the leaves with i particles (empty face
+ * roots included).  *len = max leaf size + 1; min(cap, *len) buckets are written. */
+CSFS_B200_API int csfs_b200_leaf_histogram(csfs_b200_ctx* ctx, int which, int* hist, int cap, int* len);
+
+/* --- multi-GPU building blocks: target partitioning with a caller-owned collective ----
  * The library is collective-agnostic: the CALLER owns two device buffers (sizes from
  * part_sizes) and all-reduces (sum) them between the phases (torch.distributed / NCCL
  * over NVLink in paper_2508_13550_b200/distributed.py).  Every rank, on `stream`:

@@ -11,68 +11,33 @@
 #include <string>
 #include <vector>
 
-#include "../../include/csfs_b200.h"
-#include "engine.hpp"
+#include "context.hpp"
 
 using namespace csfs_b200;
 
-struct csfs_b200_ctx {
-    int device = 0;
-    cudaStream_t own = nullptr;
-    cudaStream_t aux = nullptr;  // the upward pass, overlapped with the dual traversal
-    cudaEvent_t w_copied = nullptr;  // host API: the weights' H2D copy (on aux) is done
-    std::string err;
-    DeviceTree ttree, stree;
-    bool shared = false;
-    Scratch sc;
-    Lists lists;
-    Items items;
-    DevBuf<double> phi_near;
-    DevBuf<int> counter;
-    DevBuf<double> h_txyz, h_sxyz, h_w, h_out;  // staging for the host-pointer API
-    DevBuf<double> d_soa;
-    DevBuf<int4> d_items;
-    DevBuf<int2> d_segs;
-    DevBuf<double2> log_tab;  // fastmath.cuh table, uploaded once per context
-    DevBuf<double> bve;       // RK4 stage buffers (csfs_b200_bve_step)
-    DevBuf<int> rm_i;         // remesh buckets (csfs_b200_bve_remesh)
-    DevBuf<double> rm_d, rm_h;
-    cudaEvent_t ev[8] = {};
-    Cheb cheb{};
-    KernelSpec kspec;
-    FmmConfig cfg;
-    bool have_state = false;
-    bool have_src_tree = false;  // the last call was cstc: only the source tree exists
-    int dim = 1;
-    bool use_mutual = true;  // symmetric PP/CC evaluation (CSFS_B200_NO_SYMMETRIC=1 disables)
-    bool mutual_unit_scope = false;  // CSFS_B200_MUTUAL_SCOPE=unit: single-GPU pairs like the partitioned path
-    // multi-GPU partition state (csfs_b200_part_*)
-    bool part_planned = false;
-    cudaStream_t part_stream = nullptr;
-    DevBuf<double> phi_tree;
-    std::vector<long long> unit_b[2], unit_e[2];
-    std::vector<double> unit_cost[2];
-};
+namespace csfs_b200 {
+namespace capi {
 
 namespace {
-
 int fail(csfs_b200_ctx* c, int code, const std::string& m) {
     if (c) c->err = m;
     return code;
 }
+}  // namespace
 
-template <class F>
-int guarded(csfs_b200_ctx* c, F&& f) {
+int guarded_call(csfs_b200_ctx* c, void (*f)(void*), void* arg) {
     if (!c) return CSFS_B200_INVALID_ARGUMENT;
     try {
         CSFS_CK(cudaSetDevice(c->device));
-        f();
+        f(arg);
         c->err.clear();
         return CSFS_B200_OK;
     } catch (const InvalidArgument& e) {
         return fail(c, CSFS_B200_INVALID_ARGUMENT, e.what());
     } catch (const OutOfMemory& e) {
         return fail(c, CSFS_B200_OUT_OF_MEMORY, e.what());
+    } catch (const NcclFailure& e) {
+        return fail(c, CSFS_B200_NCCL_ERROR, e.what());
     } catch (const CudaFailure& e) {
         return fail(c, CSFS_B200_CUDA_ERROR, e.what());
     } catch (const std::exception& e) {
@@ -80,11 +45,11 @@ int guarded(csfs_b200_ctx* c, F&& f) {
     }
 }
 
-// Re-raises a nested entry point's return code as the matching exception.
 void rethrow(csfs_b200_ctx* c, int rc) {
     if (rc == CSFS_B200_OK) return;
     if (rc == CSFS_B200_INVALID_ARGUMENT) throw InvalidArgument(c->err);
     if (rc == CSFS_B200_OUT_OF_MEMORY) throw OutOfMemory(c->err);
+    if (rc == CSFS_B200_NCCL_ERROR) throw NcclFailure(c->err);
     throw CudaFailure(c->err);
 }
 
@@ -110,8 +75,6 @@ FmmConfig to_cfg(const csfs_b200_config* c) {
     return f;
 }
 
-// Validation in the reference's order: ChebyshevGrid1D (interpolation.cpp:15), then the
-// ClusterTree checks (cluster_tree.cpp:32-33), targets first.
 void validate(const FmmConfig& f, size_t nt, size_t ns) {
     if (f.degree < 1) throw InvalidArgument("interpolation degree must be positive");
     if (f.degree > kMaxNp - 1)
@@ -149,8 +112,56 @@ int count_internal(const DeviceTree& t) {
     return k;
 }
 
-// Symmetric PP evaluation (targets == sources only): pairs within one partition unit.
-// Symmetric PP pairs (k_mutual).  Scope: one GPU pairs every mirrored leaf pair
+std::unique_ptr<csfs_b200_ctx> new_context(int device) {
+    auto c = std::make_unique<csfs_b200_ctx>();
+    c->device = device;
+    int count = 0;
+    CSFS_CK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw InvalidArgument("no CUDA device " + std::to_string(device));
+    cudaDeviceProp prop{};
+    CSFS_CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        throw CudaFailure("csfs_b200 is built for sm_100a; device " + std::to_string(device) + " is sm_" +
+                          std::to_string(prop.major) + std::to_string(prop.minor));
+    CSFS_CK(cudaSetDevice(device));
+    CSFS_CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    CSFS_CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    CSFS_CK(cudaEventCreateWithFlags(&c->w_copied, cudaEventDisableTiming));
+    for (auto& e : c->ev) CSFS_CK(cudaEventCreate(&e));
+    CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
+    const char* nosym = std::getenv("CSFS_B200_NO_SYMMETRIC");
+    c->use_mutual = !(nosym && nosym[0] == '1');
+    const char* scope = std::getenv("CSFS_B200_MUTUAL_SCOPE");
+    c->mutual_unit_scope = scope && std::string(scope) == "unit";
+    std::vector<double2> tab(kLogTabWords);
+    make_log_table(tab.data());
+    c->log_tab.grow(kLogTabWords);
+    CSFS_CK(cudaMemcpy(c->log_tab.p, tab.data(), kLogTabWords * sizeof(double2), cudaMemcpyHostToDevice));
+    return c;
+}
+
+void free_context(csfs_b200_ctx* c) {
+    if (!c) return;
+    for (auto& p : c->peers) {
+        free_context(p.get());
+        p.release();
+    }
+    cudaSetDevice(c->device);
+    if (c->own) cudaStreamSynchronize(c->own);
+    if (c->aux) cudaStreamSynchronize(c->aux);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->sc.host) cudaFreeHost(c->sc.host);
+    if (c->own) cudaStreamDestroy(c->own);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->w_copied) cudaEventDestroy(c->w_copied);
+    delete c;
+}
+
+namespace {
+
+// Symmetric PP/CC pairs (k_mutual).  Scope: one GPU pairs every mirrored leaf pair
 // (`global`); the partitioned multi-GPU path restricts them to pairs inside one partition
 // unit, so no pair straddles two ranks and every rank count sums in the same order
 // (results bitwise equal across rank counts; equal to the single-GPU result to rounding).
@@ -164,14 +175,54 @@ void prepare_mutual(csfs_b200_ctx* c, cudaStream_t s, bool global) {
     c->items.mutual = c->items.n_partial > 0;
 }
 
+}  // namespace
+
+// Stats of the last run_csfmm from c->ev[0..5] (tree, upward on aux, lists, interact,
+// downward); the partitioned path overwrites the phase times it measures itself.
+void fill_stats(csfs_b200_ctx* c, csfs_b200_stats* st) {
+    cudaEvent_t* ev = c->ev;
+    const DeviceTree& T = c->ttree;
+    const DeviceTree& S = c->shared ? c->ttree : c->stree;
+    std::memset(st, 0, sizeof(*st));
+    st->t_tree_build = ev_ms(ev[0], ev[1]) * 1e-3;
+    // upward and lists overlap (both start at ev[1]); the reference's phases are
+    // sequential, so here tree + upward + traversal + downward >= total
+    st->t_upward = ev_ms(ev[1], ev[2]) * 1e-3;
+    st->t_traversal = ev_ms(ev[1], ev[4]) * 1e-3;
+    st->t_lists = ev_ms(ev[1], ev[3]) * 1e-3;
+    st->t_interact = ev_ms(ev[3], ev[4]) * 1e-3;
+    st->t_downward = ev_ms(ev[4], ev[5]) * 1e-3;
+    st->t_total = ev_ms(ev[0], ev[5]) * 1e-3;
+    st->pp = c->lists.n[0];
+    st->pc = c->lists.n[1];
+    st->cp = c->lists.n[2];
+    st->cc = c->lists.n[3];
+    st->evals_pp = c->items.pair_evals[0];
+    st->evals_pc = c->items.pair_evals[1];
+    st->evals_cp = c->items.pair_evals[2];
+    st->evals_cc = c->items.pair_evals[3];
+    st->evals_executed = c->items.pair_evals[0] + c->items.pair_evals[1] + c->items.pair_evals[2] +
+                         c->items.pair_evals[3] - (c->items.mutual ? c->items.skipped_pairs : 0);
+    st->symmetric_pairs = c->items.mutual ? c->items.n_mutual : 0;
+    st->tgt_depth = T.depth_max();
+    st->tgt_clusters = T.ncl;
+    st->tgt_leaves = T.ncl - count_internal(T);
+    st->src_depth = S.depth_max();
+    st->src_clusters = S.ncl;
+    st->src_leaves = c->shared ? st->tgt_leaves : S.ncl - count_internal(S);
+    st->shared_tree = c->shared ? 1 : 0;
+    st->n_ranks = 1;
+}
+
 // w_ready: optional event the weights' producer records (the host API copies them on
 // the aux stream while the tree levels are built).
 void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
                const double* sw, size_t ns, const KernelSpec& ks, const FmmConfig& f, double* out,
-               csfs_b200_stats* st, cudaStream_t s, cudaEvent_t w_ready = nullptr) {
+               csfs_b200_stats* st, cudaStream_t s, cudaEvent_t w_ready) {
     validate(f, nt, ns);
     c->have_state = false;
     c->have_src_tree = false;
+    c->part_planned = false;
     c->kspec = ks;
     c->cfg = f;
     c->dim = ks.out_dim();
@@ -213,43 +264,75 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     CSFS_CK(cudaEventRecord(ev[5], s));
     CSFS_CK(cudaEventSynchronize(ev[5]));
     c->have_state = true;
-
-    if (st) {
-        std::memset(st, 0, sizeof(*st));
-        st->t_tree_build = ev_ms(ev[0], ev[1]) * 1e-3;
-        // upward and lists overlap (both start at ev[1]); the reference's phases are
-        // sequential, so here tree + upward + traversal + downward >= total
-        st->t_upward = ev_ms(ev[1], ev[2]) * 1e-3;
-        st->t_traversal = ev_ms(ev[1], ev[4]) * 1e-3;
-        st->t_lists = ev_ms(ev[1], ev[3]) * 1e-3;
-        st->t_interact = ev_ms(ev[3], ev[4]) * 1e-3;
-        st->t_downward = ev_ms(ev[4], ev[5]) * 1e-3;
-        st->t_total = ev_ms(ev[0], ev[5]) * 1e-3;
-        st->pp = c->lists.n[0];
-        st->pc = c->lists.n[1];
-        st->cp = c->lists.n[2];
-        st->cc = c->lists.n[3];
-        st->evals_pp = c->items.pair_evals[0];
-        st->evals_pc = c->items.pair_evals[1];
-        st->evals_cp = c->items.pair_evals[2];
-        st->evals_cc = c->items.pair_evals[3];
-        st->evals_executed = c->items.pair_evals[0] + c->items.pair_evals[1] + c->items.pair_evals[2] +
-                             c->items.pair_evals[3] - (c->items.mutual ? c->items.skipped_pairs : 0);
-        st->symmetric_pairs = c->items.mutual ? c->items.n_mutual : 0;
-        st->tgt_depth = T.depth_max();
-        st->tgt_clusters = T.ncl;
-        st->tgt_leaves = T.ncl - count_internal(T);
-        st->src_depth = S.depth_max();
-        st->src_clusters = S.ncl;
-        st->src_leaves = c->shared ? st->tgt_leaves : S.ncl - count_internal(S);
-        st->shared_tree = c->shared ? 1 : 0;
-    }
+    if (st) fill_stats(c, st);
 }
+
+void part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz, const double* sw, size_t ns,
+               const KernelSpec& ks, const FmmConfig& f, cudaStream_t s) {
+    validate(f, nt, ns);
+    c->have_state = false;
+    c->have_src_tree = false;
+    c->part_planned = false;
+    c->part_stream = s;
+    c->kspec = ks;
+    c->cfg = f;
+    c->dim = ks.out_dim();
+    c->cheb = make_cheb(f.degree);
+    const int n0 = f.resolved_n0();
+    c->shared = (nt == ns) && device_equal(txyz, sxyz, nt * 3 * sizeof(double), c->sc, s);
+    DeviceTree& T = c->ttree;
+    DeviceTree& S = c->shared ? c->ttree : c->stree;
+    build_tree(T, c->sc, txyz, c->shared ? sw : nullptr, (long long)nt, f.degree, n0, f.shrink, c->cheb, s);
+    if (!c->shared) build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s);
+    dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
+    build_items(T, S, c->lists, c->items, c->sc, s);
+    prepare_mutual(c, s, false);  // unit scope: the same pairs for every rank count
+    // partition units: depth-1 subtrees plus unsplit roots, in tree order
+    for (int w = 0; w < 2; ++w) {
+        const DeviceTree& t = (w == 0 || c->shared) ? T : S;
+        partition_units(t, c->unit_b[w], c->unit_e[w]);
+        c->unit_cost[w].assign(c->unit_b[w].size(), 0.0);
+        if (w == 1)
+            for (size_t i = 0; i < c->unit_b[1].size(); ++i)
+                c->unit_cost[1][i] = double(c->unit_e[1][i] - c->unit_b[1][i]);
+    }
+    {
+        const int ni = c->items.n_items;
+        std::vector<int> anchor(ni);
+        std::vector<double> cost(ni);
+        if (ni) {
+            CSFS_CK(cudaMemcpy(anchor.data(), c->items.anchor.p, ni * sizeof(int), cudaMemcpyDeviceToHost));
+            CSFS_CK(cudaMemcpy(cost.data(), c->items.cost.p, ni * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        const auto& ub = c->unit_b[0];
+        for (int i = 0; i < ni; ++i) {
+            if (anchor[i] < 0) continue;
+            const size_t u = size_t(std::upper_bound(ub.begin(), ub.end(), (long long)anchor[i]) - ub.begin()) - 1;
+            c->unit_cost[0][u] += cost[i];
+        }
+    }
+    c->part_planned = true;
+}
+
+}  // namespace capi
+}  // namespace csfs_b200
+
+using namespace csfs_b200::capi;
+
+namespace {
 
 // Device-pointer entry points run on the caller's stream; NULL is CUDA's legacy default
 // stream (what torch reports as cuda_stream == 0), never a private stream, so work stays
 // ordered with the caller's producers and consumers.
 cudaStream_t pick(csfs_b200_ctx*, void* stream) { return static_cast<cudaStream_t>(stream); }
+
+// csfmm on a context: one device, or the partitioned evaluation over its group.
+void csfmm_any(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz, const double* sw, size_t ns,
+               const KernelSpec& ks, const FmmConfig& f, double* out, csfs_b200_stats* st, cudaStream_t s,
+               cudaEvent_t w_ready = nullptr) {
+    if (c->mode == csfs_b200_ctx::Mode::Single) run_csfmm(c, txyz, nt, sxyz, sw, ns, ks, f, out, st, s, w_ready);
+    else run_csfmm_group(c, txyz, nt, sxyz, sw, ns, ks, f, out, st, s, w_ready);
+}
 
 struct HostTree {
     std::vector<int> face, depth, begin, end, parent, nchild, ref, inv;
@@ -291,52 +374,19 @@ extern "C" {
 int csfs_b200_create(csfs_b200_ctx** out, int device) {
     if (!out) return CSFS_B200_INVALID_ARGUMENT;
     *out = nullptr;
-    auto c = std::make_unique<csfs_b200_ctx>();
-    c->device = device;
-    int rc = guarded(c.get(), [&] {
-        int count = 0;
-        CSFS_CK(cudaGetDeviceCount(&count));
-        if (device < 0 || device >= count) throw InvalidArgument("no CUDA device " + std::to_string(device));
-        cudaDeviceProp prop{};
-        CSFS_CK(cudaGetDeviceProperties(&prop, device));
-        if (prop.major != 10)
-            throw CudaFailure("csfs_b200 is built for sm_100a; device " + std::to_string(device) +
-                              " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
-        CSFS_CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
-        CSFS_CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
-        CSFS_CK(cudaEventCreateWithFlags(&c->w_copied, cudaEventDisableTiming));
-        for (auto& e : c->ev) CSFS_CK(cudaEventCreate(&e));
-        CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
-        const char* nosym = std::getenv("CSFS_B200_NO_SYMMETRIC");
-        c->use_mutual = !(nosym && nosym[0] == '1');
-        const char* scope = std::getenv("CSFS_B200_MUTUAL_SCOPE");
-        c->mutual_unit_scope = scope && std::string(scope) == "unit";
-        std::vector<double2> tab(kLogTabWords);
-        make_log_table(tab.data());
-        c->log_tab.grow(kLogTabWords);
-        CSFS_CK(cudaMemcpy(c->log_tab.p, tab.data(), kLogTabWords * sizeof(double2), cudaMemcpyHostToDevice));
-    });
-    if (rc != CSFS_B200_OK) {
-        // keep the context alive only to report the error? The caller gets NULL.
-        return rc;
+    try {
+        *out = new_context(device).release();
+        return CSFS_B200_OK;
+    } catch (const InvalidArgument&) {
+        return CSFS_B200_INVALID_ARGUMENT;
+    } catch (const OutOfMemory&) {
+        return CSFS_B200_OUT_OF_MEMORY;
+    } catch (const std::exception&) {
+        return CSFS_B200_CUDA_ERROR;
     }
-    *out = c.release();
-    return CSFS_B200_OK;
 }
 
-void csfs_b200_destroy(csfs_b200_ctx* c) {
-    if (!c) return;
-    cudaSetDevice(c->device);
-    if (c->own) cudaStreamSynchronize(c->own);
-    for (auto& e : c->ev)
-        if (e) cudaEventDestroy(e);
-    if (c->aux) cudaStreamSynchronize(c->aux);
-    if (c->sc.host) cudaFreeHost(c->sc.host);
-    if (c->own) cudaStreamDestroy(c->own);
-    if (c->aux) cudaStreamDestroy(c->aux);
-    if (c->w_copied) cudaEventDestroy(c->w_copied);
-    delete c;
-}
+void csfs_b200_destroy(csfs_b200_ctx* c) { free_context(c); }
 
 const char* csfs_b200_last_error(const csfs_b200_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
@@ -345,7 +395,7 @@ int csfs_b200_csfmm_device(csfs_b200_ctx* c, const double* txyz, size_t nt, cons
                            const csfs_b200_config* cfg, double* out, csfs_b200_stats* st,
                            void* stream) {
     return guarded(c, [&] {
-        run_csfmm(c, txyz, nt, sxyz, sw, ns, to_spec(k), to_cfg(cfg), out, st, pick(c, stream));
+        csfmm_any(c, txyz, nt, sxyz, sw, ns, to_spec(k), to_cfg(cfg), out, st, pick(c, stream));
     });
 }
 
@@ -373,7 +423,7 @@ int csfs_b200_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const doubl
         CSFS_CK(cudaEventRecord(c->w_copied, c->aux));
         const size_t nout = nt * size_t(ks.out_dim());
         c->h_out.grow(nout);
-        run_csfmm(c, c->h_txyz.p, nt, dsrc, c->h_w.p, ns, ks, f, c->h_out.p, st, s, c->w_copied);
+        csfmm_any(c, c->h_txyz.p, nt, dsrc, c->h_w.p, ns, ks, f, c->h_out.p, st, s, c->w_copied);
         CSFS_CK(cudaMemcpyAsync(out, c->h_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaStreamSynchronize(s));
     });
@@ -466,6 +516,25 @@ int csfs_b200_tree_export(csfs_b200_ctx* c, int which, int* perm, int* ints, dou
                     for (int f = 0; f < 3; ++f)
                         proxy[(size_t(h.ref[i]) * t.npp + k) * 3 + f] = q[f][size_t(i) * t.npp + k];
         }
+    });
+}
+
+int csfs_b200_leaf_histogram(csfs_b200_ctx* c, int which, int* hist, int cap, int* len) {
+    return guarded(c, [&] {
+        const DeviceTree& t = which_tree(c, which);
+        std::vector<int> b(t.ncl), e(t.ncl), nch(t.ncl);
+        CSFS_CK(cudaMemcpy(b.data(), t.begin.p, t.ncl * sizeof(int), cudaMemcpyDeviceToHost));
+        CSFS_CK(cudaMemcpy(e.data(), t.end.p, t.ncl * sizeof(int), cudaMemcpyDeviceToHost));
+        CSFS_CK(cudaMemcpy(nch.data(), t.nchild.p, t.ncl * sizeof(int), cudaMemcpyDeviceToHost));
+        std::vector<int> h;
+        for (int i = 0; i < t.ncl; ++i) {
+            if (nch[i] > 0) continue;
+            const int n = e[i] - b[i];
+            if (int(h.size()) <= n) h.resize(n + 1, 0);
+            ++h[n];
+        }
+        if (len) *len = int(h.size());
+        for (int i = 0; i < std::min<int>(cap, int(h.size())); ++i) hist[i] = h[i];
     });
 }
 
@@ -607,7 +676,7 @@ int csfs_b200_bve_step_device(csfs_b200_ctx* c, double* xyz, double* zeta, const
         const double hs[3] = {0.5 * dt, 0.5 * dt, dt};
         for (int q = 0; q < 4; ++q) {
             const double* P = q == 0 ? x0 : pos;
-            run_csfmm(c, P, n, P, w, n, ks, f, k[q], stage_stats ? stage_stats + q : nullptr, s);
+            csfmm_any(c, P, n, P, w, n, ks, f, k[q], stage_stats ? stage_stats + q : nullptr, s);
             if (q < 3) bve_advance(N, x0, zeta, k[q], hs[q], omega, areas, pos, zs, w, s);
         }
         bve_final(N, xyz, zeta, k[0], k[1], k[2], k[3], dt, omega, s);
@@ -683,54 +752,7 @@ int csfs_b200_bve_remesh(csfs_b200_ctx* c, double* xyz, double* zeta, double* tr
 int csfs_b200_part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz,
                         const double* sw, size_t ns, const csfs_b200_kernel* k,
                         const csfs_b200_config* cfg, void* stream) {
-    return guarded(c, [&] {
-        const KernelSpec ks = to_spec(k);
-        const FmmConfig f = to_cfg(cfg);
-        validate(f, nt, ns);
-        cudaStream_t s = pick(c, stream);
-        c->have_state = false;
-        c->have_src_tree = false;
-        c->part_planned = false;
-        c->part_stream = s;
-        c->kspec = ks;
-        c->cfg = f;
-        c->dim = ks.out_dim();
-        c->cheb = make_cheb(f.degree);
-        const int n0 = f.resolved_n0();
-        c->shared = (nt == ns) && device_equal(txyz, sxyz, nt * 3 * sizeof(double), c->sc, s);
-        DeviceTree& T = c->ttree;
-        DeviceTree& S = c->shared ? c->ttree : c->stree;
-        build_tree(T, c->sc, txyz, c->shared ? sw : nullptr, (long long)nt, f.degree, n0, f.shrink, c->cheb, s);
-        if (!c->shared) build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s);
-        dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
-        build_items(T, S, c->lists, c->items, c->sc, s);
-        prepare_mutual(c, s, false);  // unit scope: the same pairs for every rank count
-        // partition units: depth-1 subtrees plus unsplit roots, in tree order
-        for (int w = 0; w < 2; ++w) {
-            const DeviceTree& t = (w == 0 || c->shared) ? T : S;
-            partition_units(t, c->unit_b[w], c->unit_e[w]);
-            c->unit_cost[w].assign(c->unit_b[w].size(), 0.0);
-            if (w == 1)
-                for (size_t i = 0; i < c->unit_b[1].size(); ++i)
-                    c->unit_cost[1][i] = double(c->unit_e[1][i] - c->unit_b[1][i]);
-        }
-        {
-            const int ni = c->items.n_items;
-            std::vector<int> anchor(ni);
-            std::vector<double> cost(ni);
-            if (ni) {
-                CSFS_CK(cudaMemcpy(anchor.data(), c->items.anchor.p, ni * sizeof(int), cudaMemcpyDeviceToHost));
-                CSFS_CK(cudaMemcpy(cost.data(), c->items.cost.p, ni * sizeof(double), cudaMemcpyDeviceToHost));
-            }
-            const auto& ub = c->unit_b[0];
-            for (int i = 0; i < ni; ++i) {
-                if (anchor[i] < 0) continue;
-                const size_t u = size_t(std::upper_bound(ub.begin(), ub.end(), (long long)anchor[i]) - ub.begin()) - 1;
-                c->unit_cost[0][u] += cost[i];
-            }
-        }
-        c->part_planned = true;
-    });
+    return guarded(c, [&] { part_plan(c, txyz, nt, sxyz, sw, ns, to_spec(k), to_cfg(cfg), pick(c, stream)); });
 }
 
 int csfs_b200_part_units(csfs_b200_ctx* c, int which, int* n_units, long long* begin, long long* end,

@@ -100,7 +100,8 @@ class SumStats(C.Structure):  # summation.hpp:44-53 + B200 extras
                 ("t_lists", C.c_double), ("t_interact", C.c_double),
                 ("evals_pp", C.c_uint64), ("evals_pc", C.c_uint64), ("evals_cp", C.c_uint64),
                 ("evals_cc", C.c_uint64), ("shared_tree", C.c_int),
-                ("evals_executed", C.c_uint64), ("symmetric_pairs", C.c_int)]
+                ("evals_executed", C.c_uint64), ("symmetric_pairs", C.c_int),
+                ("n_ranks", C.c_int), ("t_exchange", C.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -170,6 +171,12 @@ def lib() -> C.CDLL:
         L.csfs_b200_part_upward.argtypes = [P, C.c_longlong, C.c_longlong, P]
         L.csfs_b200_part_eval.argtypes = [P, C.c_longlong, C.c_longlong, P, P]
         L.csfs_b200_part_finish.argtypes = [P, P, P]
+        L.csfs_b200_create_multi.argtypes = [C.POINTER(P), I, P]
+        L.csfs_b200_create_rank.argtypes = [C.POINTER(P), I, I, I, C.c_char_p]
+        L.csfs_b200_create_emulated.argtypes = [C.POINTER(P), I, I]
+        L.csfs_b200_nccl_unique_id.argtypes = [C.c_char_p]
+        L.csfs_b200_group_info.argtypes = [P, C.POINTER(I), C.POINTER(I), P, P, P]
+        L.csfs_b200_leaf_histogram.argtypes = [P, I, P, I, C.POINTER(I)]
         _lib = L
     return _lib
 
@@ -191,18 +198,90 @@ def _cconfig(c: TraversalConfig) -> _CConfig:
     return _CConfig(float(c.mac), int(c.degree), int(c.n0), 1 if c.shrink else 0)
 
 
-class Engine:
-    """One csfs_b200_ctx: one device, one stream, reusable device buffers."""
+NCCL_ID_BYTES = 128  # CSFS_B200_NCCL_ID_BYTES
 
-    def __init__(self, device: int = 0):
+
+def nccl_unique_id() -> bytes:
+    """csfs_b200_nccl_unique_id: rank 0 makes it, the other ranks receive it (any channel)."""
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    rc = lib().csfs_b200_nccl_unique_id(buf)
+    if rc != OK:
+        raise RuntimeError(f"csfs_b200_nccl_unique_id failed with code {rc}")
+    return buf.raw
+
+
+class Engine:
+    """One csfs_b200_ctx: one device (default), or a multi-GPU group whose csfmm calls run
+    the target-partitioned evaluation with NCCL exchanges (include/csfs_b200.h):
+
+      Engine(device)                          one GPU
+      Engine.multi(num_gpus, device_ids)      one process, N devices (ncclCommInitAll)
+      Engine.rank(device, nranks, rank, id)   one process per GPU (torchrun), NCCL unique id
+      Engine.emulated(device, nranks)         N ranks on one device (partition parity tests)
+    """
+
+    def __init__(self, device: int = 0, _handle=None):
         self._lib = lib()
-        h = C.c_void_p()
-        rc = self._lib.csfs_b200_create(C.byref(h), int(device))
-        if rc != OK:
-            raise RuntimeError(f"csfs_b200_create(device={device}) failed with code {rc} "
-                               "(needs an sm_100 GPU; there is no CPU fallback)")
-        self._h = h
+        if _handle is None:
+            h = C.c_void_p()
+            rc = self._lib.csfs_b200_create(C.byref(h), int(device))
+            if rc != OK:
+                raise RuntimeError(f"csfs_b200_create(device={device}) failed with code {rc} "
+                                   "(needs an sm_100 GPU; there is no CPU fallback)")
+            _handle = h
+        self._h = _handle
         self.device = device
+
+    @classmethod
+    def _made(cls, rc: int, h, device: int, what: str) -> "Engine":
+        if rc != OK:
+            raise RuntimeError(f"{what} failed with code {rc} (3 = NCCL error; needs sm_100 GPUs)")
+        return cls(device, _handle=h)
+
+    @classmethod
+    def multi(cls, num_gpus: int, device_ids=None) -> "Engine":
+        h = C.c_void_p()
+        ids = None
+        if device_ids is not None:
+            ids = (C.c_int * num_gpus)(*[int(d) for d in device_ids])
+        rc = lib().csfs_b200_create_multi(C.byref(h), int(num_gpus), ids)
+        return cls._made(rc, h, int(device_ids[0]) if device_ids is not None else 0,
+                         f"csfs_b200_create_multi({num_gpus})")
+
+    @classmethod
+    def rank(cls, device: int, nranks: int, rank: int, unique_id: bytes) -> "Engine":
+        if len(unique_id) != NCCL_ID_BYTES:
+            raise ValueError("the NCCL unique id has 128 bytes")
+        h = C.c_void_p()
+        rc = lib().csfs_b200_create_rank(C.byref(h), int(device), int(nranks), int(rank), unique_id)
+        return cls._made(rc, h, device, f"csfs_b200_create_rank(rank {rank} of {nranks})")
+
+    @classmethod
+    def emulated(cls, device: int, nranks: int) -> "Engine":
+        h = C.c_void_p()
+        rc = lib().csfs_b200_create_emulated(C.byref(h), int(device), int(nranks))
+        return cls._made(rc, h, device, f"csfs_b200_create_emulated({nranks})")
+
+    def group_info(self) -> dict:
+        n, r = C.c_int(), C.c_int()
+        self._check(self._lib.csfs_b200_group_info(self._h, C.byref(n), C.byref(r), None, None, None))
+        dev = np.empty(n.value, np.int32)
+        self._check(self._lib.csfs_b200_group_info(self._h, None, None, _ptr(dev), None, None))
+        info = {"nranks": n.value, "rank": r.value, "devices": dev.tolist()}
+        tr = np.empty(2 * n.value, np.int64)
+        sr = np.empty(2 * n.value, np.int64)
+        if self._lib.csfs_b200_group_info(self._h, None, None, None, _ptr(tr), _ptr(sr)) == OK and n.value > 1:
+            info["target_ranges"] = tr.reshape(-1, 2).tolist()
+            info["source_ranges"] = sr.reshape(-1, 2).tolist()
+        return info
+
+    def leaf_histogram(self, which: int) -> list[int]:
+        """TreeStats::leaf_size_histogram of the last call's target (0) / source (1) tree."""
+        n = C.c_int()
+        self._check(self._lib.csfs_b200_leaf_histogram(self._h, which, None, 0, C.byref(n)))
+        h = np.zeros(n.value, np.int32)
+        self._check(self._lib.csfs_b200_leaf_histogram(self._h, which, _ptr(h), n.value, C.byref(n)))
+        return h.tolist()
 
     def close(self):
         if getattr(self, "_h", None):
@@ -223,6 +302,8 @@ class Engine:
             raise ValueError(msg)
         if rc == OUT_OF_MEMORY:
             raise MemoryError(msg)
+        if rc == NCCL_ERROR:
+            raise RuntimeError(f"csfs_b200 NCCL error: {msg}")
         raise RuntimeError(f"csfs_b200 error {rc}: {msg}")
 
     # --- reference API mirror --------------------------------------------------------

@@ -11,12 +11,15 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from ncu_summary import summarise  # noqa: E402
+
+from paper_2508_13550_b200.srchash import eval_kernel_sha256  # noqa: E402
 
 
 def main(tag, out):
     bench = json.loads(open(f"gpurun_out/bench_{tag}.json").read().strip().splitlines()[-1])
-    L = bench["roofline"]["pair_evals_per_launch"]
+    L = bench["roofline"]["list_pair_evals_per_launch"]
     E = bench["roofline"]["executed_pair_evals_per_launch"]
     pm, pi = L - E, 2 * E - L
     ks = summarise(f"gpurun_out/prof_{tag}_mut.csv", {"k_mutual": pm}, f"ncu --set full (prof_{tag}_mut, kernel replay)")
@@ -34,6 +37,7 @@ def main(tag, out):
            "fp64_inst_per_pair": sum(k["fp64_inst_per_pair"] * k["pair_evals"] for k in ks) / pe,
            "fp64_tflops_executed": fl / dur / 1e9,
            "fp64_pipe_active_pct": sum(k["fp64_pipe_active_pct"] * k["duration_ms"] for k in ks) / dur,
+           "source_sha256": eval_kernel_sha256(),
            "kernels": ks}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps({k: v for k, v in res.items() if k != "kernels"}))
