@@ -159,6 +159,63 @@ CSFS_B200_API int csfs_b200_lists_export(csfs_b200_ctx* ctx, long long* counts, 
 /* Source-tree proxy weights after the upward pass, ncl x (p+1)^2, reference id order. */
 CSFS_B200_API int csfs_b200_proxy_weights_export(csfs_b200_ctx* ctx, double* pw);
 
+/* --- the stepwise API: the pieces of csfmm_sum on trees the CALLER holds -------------------
+ * The reference exposes its pipeline piece by piece (cluster_tree.hpp:52-81,
+ * summation.hpp:66-102) and its tests drive the pieces on trees they modify in between
+ * (acceptance.cpp:229-280).  A caller's tree — the reference's ClusterTree — is handed
+ * over as plain arrays in REFERENCE cluster ids (exactly what csfs_b200_tree_export /
+ * _tree_particles return for a tree this library built); every call uploads what it reads.
+ * The C++ shim (host/csfs_b200_shim.cpp) marshals csfs::ClusterTree into this form. */
+typedef struct {
+    size_t n;              /* particles */
+    int n_clusters;        /* clusters 0..5 are the face roots */
+    int degree;            /* interpolation degree (proxy grid (degree+1)^2) */
+    const int* perm;       /* n: tree order -> input index (ClusterTree::perm) */
+    const double* xyz;     /* n x 3: positions in tree order (ClusterTree::points) */
+    const double* xi;      /* n: face coordinates in tree order (ClusterTree::xi / eta) */
+    const double* eta;
+    const int* ints;       /* n_clusters x 10: face, begin, end, parent, depth, child_count,
+                              children[4] (-1 padded) — the layout of csfs_b200_tree_export */
+    const double* dbls;    /* n_clusters x 8: xi0, xi1, eta0, eta1 (bounds), cx, cy, cz, radius */
+    const double* proxy;   /* n_clusters x (degree+1)^2 x 3: CellInterpolant::proxy_points */
+} csfs_b200_tree_desc;
+
+/* ClusterTree(particles, degree, n0, shrink) (cluster_tree.cpp:29-147) on the device;
+ * afterwards csfs_b200_tree_info / _tree_export / _tree_particles with which = 0 return
+ * it (reference ids).  The reference's std::invalid_argument messages as code 1. */
+CSFS_B200_API int csfs_b200_tree_build(csfs_b200_ctx* ctx, const double* xyz, size_t n, int degree, int n0,
+                                       int shrink, int* n_clusters, int* depth);
+/* Tree-order positions (n x 3), xi and eta (n each) of a tree: which 0 target / 1 source
+ * of the last call (or the tree_build tree).  Any pointer may be NULL. */
+CSFS_B200_API int csfs_b200_tree_particles(csfs_b200_ctx* ctx, int which, double* xyz, double* xi, double* eta);
+/* upward_pass(tree, weights) (cluster_tree.cpp:163-220): w in input order; pw receives
+ * n_clusters x (degree+1)^2 proxy weights in reference ids. */
+CSFS_B200_API int csfs_b200_upward_tree(csfs_b200_ctx* ctx, const csfs_b200_tree_desc* tree, const double* w,
+                                        double* pw);
+/* downward_pass(tree, out_dim, out) (cluster_tree.cpp:228-283): qphi (n_clusters x
+ * (degree+1)^2 x dim, reference ids) is pushed parents -> children IN PLACE (like the
+ * reference's tree) and interpolated to the particles, ADDED into out (n x dim, input
+ * order). */
+CSFS_B200_API int csfs_b200_downward_tree(csfs_b200_ctx* ctx, const csfs_b200_tree_desc* tree, int dim,
+                                          double* qphi, double* out);
+/* dual_tree_traversal(targets, sources, mac, n0) (summation.cpp:163-203): counts[4] =
+ * |pp|,|pc|,|cp|,|cc|; then csfs_b200_lists_export returns the (t, s) sets in reference
+ * ids, sorted (the reference emits them in its LIFO visiting order; the sets are equal). */
+CSFS_B200_API int csfs_b200_traversal_tree(csfs_b200_ctx* ctx, const csfs_b200_tree_desc* targets,
+                                           const csfs_b200_tree_desc* sources, double mac, int n0,
+                                           long long* counts);
+/* evaluate_pp / evaluate_pc / accumulate_cp_cc (summation.cpp:205-306) for the given
+ * lists ((t, s) int pairs, reference ids; any count may be 0): PP and PC results are ADDED
+ * into out (targets' n x dim, input order), CP and CC into qphi (targets' n_clusters x
+ * (degree+1)^2 x dim).  w: sources' weights, input order (PP, CP); src_pw: sources' proxy
+ * weights (n_clusters x (degree+1)^2, PC, CC).  Each target sums its list entries in the
+ * (type, source id) order. */
+CSFS_B200_API int csfs_b200_evaluate_tree(csfs_b200_ctx* ctx, const csfs_b200_tree_desc* targets,
+                                          const csfs_b200_tree_desc* sources, const double* w, const double* src_pw,
+                                          const csfs_b200_kernel* kernel, const int* pp, long long n_pp,
+                                          const int* pc, long long n_pc, const int* cp, long long n_cp,
+                                          const int* cc, long long n_cc, double* out, double* qphi);
+
 /* --- multi-GPU contexts: csfs_b200_csfmm / _csfmm_device / _bve_step on them run the
  * target-partitioned CSFMM over every rank of the group, with the proxy-weight and
  * potential exchanges as NCCL all-gathers over NVLink (partition.cu).  Results are bitwise

@@ -222,6 +222,9 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     validate(f, nt, ns);
     c->have_state = false;
     c->have_src_tree = false;
+    c->have_tree = false;
+    c->ref_of[0].clear();
+    c->ref_of[1].clear();
     c->part_planned = false;
     c->kspec = ks;
     c->cfg = f;
@@ -272,6 +275,9 @@ void part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     validate(f, nt, ns);
     c->have_state = false;
     c->have_src_tree = false;
+    c->have_tree = false;
+    c->ref_of[0].clear();
+    c->ref_of[1].clear();
     c->part_planned = false;
     c->part_stream = s;
     c->kspec = ks;
@@ -339,7 +345,7 @@ struct HostTree {
     std::vector<int4> child;
 };
 
-HostTree fetch_topology(const DeviceTree& t) {
+HostTree fetch_topology(const DeviceTree& t, const std::vector<int>* ref_of = nullptr) {
     HostTree h;
     const int n = t.ncl;
     auto get = [&](std::vector<int>& v, const int* p) {
@@ -354,7 +360,7 @@ HostTree fetch_topology(const DeviceTree& t) {
     get(h.nchild, t.nchild);
     h.child.resize(n);
     CSFS_CK(cudaMemcpy(h.child.data(), t.child.p, n * sizeof(int4), cudaMemcpyDeviceToHost));
-    h.ref = reference_ids(h.parent, h.depth, h.child, h.nchild);
+    h.ref = (ref_of && !ref_of->empty()) ? *ref_of : reference_ids(h.parent, h.depth, h.child, h.nchild);
     h.inv.assign(n, -1);
     for (int i = 0; i < n; ++i) h.inv[h.ref[i]] = i;
     return h;
@@ -363,6 +369,7 @@ HostTree fetch_topology(const DeviceTree& t) {
 const DeviceTree& which_tree(const csfs_b200_ctx* c, int which) {
     if (which != 0 && which != 1) throw InvalidArgument("which must be 0 (target) or 1 (source)");
     if (c->have_src_tree && which == 1) return c->stree;  // after cstc
+    if (c->have_tree && which == 0) return c->ttree;      // after tree_build
     if (!c->have_state) throw InvalidArgument("no csfmm state: call csfs_b200_csfmm first");
     return (which == 0 || c->shared) ? c->ttree : c->stree;
 }
@@ -467,8 +474,9 @@ int csfs_b200_direct(csfs_b200_ctx* c, const double* txyz, size_t nt, const doub
 int csfs_b200_tree_info(const csfs_b200_ctx* c, int which, int* ncl, int* depth, size_t* n, int* npp) {
     if (!c) return CSFS_B200_INVALID_ARGUMENT;
     const bool src_only = c->have_src_tree && which == 1;
-    if ((!c->have_state && !src_only) || (which != 0 && which != 1)) return CSFS_B200_INVALID_ARGUMENT;
-    const DeviceTree& t = src_only ? c->stree : (which == 0 || c->shared) ? c->ttree : c->stree;
+    const bool tree_only = c->have_tree && which == 0;
+    if ((!c->have_state && !src_only && !tree_only) || (which != 0 && which != 1)) return CSFS_B200_INVALID_ARGUMENT;
+    const DeviceTree& t = src_only ? c->stree : tree_only ? c->ttree : (which == 0 || c->shared) ? c->ttree : c->stree;
     if (ncl) *ncl = t.ncl;
     if (depth) *depth = t.depth_max();
     if (n) *n = size_t(t.n);
@@ -479,7 +487,7 @@ int csfs_b200_tree_info(const csfs_b200_ctx* c, int which, int* ncl, int* depth,
 int csfs_b200_tree_export(csfs_b200_ctx* c, int which, int* perm, int* ints, double* dbls, double* proxy) {
     return guarded(c, [&] {
         const DeviceTree& t = which_tree(c, which);
-        const HostTree h = fetch_topology(t);
+        const HostTree h = fetch_topology(t, &c->ref_of[(&t == &c->stree) ? 1 : 0]);
         const int n = t.ncl;
         if (perm) CSFS_CK(cudaMemcpy(perm, t.perm.p, t.n * sizeof(int), cudaMemcpyDeviceToHost));
         if (ints) {
@@ -541,8 +549,8 @@ int csfs_b200_leaf_histogram(csfs_b200_ctx* c, int which, int* hist, int cap, in
 int csfs_b200_lists_export(csfs_b200_ctx* c, long long* counts, int* pp, int* pc, int* cp, int* cc) {
     return guarded(c, [&] {
         if (!c->have_state) throw InvalidArgument("no csfmm state: call csfs_b200_csfmm first");
-        const HostTree ht = fetch_topology(c->ttree);
-        const HostTree hs = c->shared ? ht : fetch_topology(c->stree);
+        const HostTree ht = fetch_topology(c->ttree, &c->ref_of[0]);
+        const HostTree hs = c->shared ? ht : fetch_topology(c->stree, &c->ref_of[1]);
         int* outs[4] = {pp, pc, cp, cc};
         for (int k = 0; k < 4; ++k) {
             if (counts) counts[k] = c->lists.n[k];
@@ -564,7 +572,7 @@ int csfs_b200_lists_export(csfs_b200_ctx* c, long long* counts, int* pp, int* pc
 int csfs_b200_proxy_weights_export(csfs_b200_ctx* c, double* pw) {
     return guarded(c, [&] {
         const DeviceTree& s = which_tree(c, 1);
-        const HostTree h = fetch_topology(s);
+        const HostTree h = fetch_topology(s, &c->ref_of[(&s == &c->stree) ? 1 : 0]);
         const size_t nq = size_t(s.ncl) * s.npp;
         std::vector<double> q(nq);
         CSFS_CK(cudaMemcpy(q.data(), s.qw.p, nq * sizeof(double), cudaMemcpyDeviceToHost));
@@ -591,6 +599,9 @@ int csfs_b200_cstc_device(csfs_b200_ctx* c, const double* txyz, size_t nt, const
         cudaStream_t s = pick(c, stream);
         c->have_state = false;
         c->have_src_tree = false;
+        c->have_tree = false;
+        c->ref_of[0].clear();
+        c->ref_of[1].clear();
         c->cheb = make_cheb(f.degree);
         const int n0 = f.resolved_n0();
         cudaEvent_t* ev = c->ev;

@@ -44,6 +44,10 @@ struct csfs_b200_ctx {
     csfs_b200::FmmConfig cfg;
     bool have_state = false;
     bool have_src_tree = false;  // the last call was cstc: only the source tree exists
+    bool have_tree = false;      // the last call was csfs_b200_tree_build: only ttree exists
+    // trees uploaded by the stepwise API: reference id of every internal cluster (target,
+    // source); empty = trees built here (ids reconstructed by reference_ids)
+    std::vector<int> ref_of[2];
     int dim = 1;
     bool use_mutual = true;  // symmetric PP/CC evaluation (CSFS_B200_NO_SYMMETRIC=1 disables)
     bool mutual_unit_scope = false;  // CSFS_B200_MUTUAL_SCOPE=unit: single-GPU pairs like the partitioned path

@@ -174,6 +174,8 @@ struct PhaseTimes {
 void build_tree(DeviceTree& tree, Scratch& sc, const double* xyz, const double* w, long long n,
                 int degree, int n0, bool shrink, const Cheb& cheb, cudaStream_t s,
                 cudaEvent_t w_ready = nullptr);
+// qrad (max centre-to-proxy distance) of every cluster, for trees uploaded by the stepwise API.
+void tree_proxy_radii(DeviceTree& t, cudaStream_t s);
 // Device byte comparison (targets == sources detection).
 bool device_equal(const void* a, const void* b, size_t bytes, Scratch& sc, cudaStream_t s);
 

@@ -893,6 +893,14 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
     CSFS_LAUNCH_CHECK();
 }
 
+void tree_proxy_radii(DeviceTree& t, cudaStream_t s) {
+    t.qrad.grow(std::max(t.ncl, 1));
+    if (t.ncl == 0) return;
+    k_qrad<<<ceil_div((long long)t.ncl * 32, kThreads), kThreads, 0, s>>>(t.ncl, t.npp, t.cx, t.cy, t.cz, t.qx, t.qy,
+                                                                          t.qz, t.qrad);
+    CSFS_LAUNCH_CHECK();
+}
+
 bool device_equal(const void* a, const void* b, size_t bytes, Scratch& sc, cudaStream_t s) {
     if (a == b) return true;
     sc.counters.grow(8);
