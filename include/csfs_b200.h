@@ -70,6 +70,8 @@ typedef struct {
     int symmetric_pairs;      /* PP leaf / CC cluster pairs evaluated once for both directions */
     int n_ranks;              /* ranks that evaluated the call (1: one GPU) */
     double t_exchange;        /* seconds in the two NCCL all-gathers (rank 0; 0 on one GPU) */
+    int traversal_fallback;   /* 1: a host-free traversal sweep overflowed its buffers and the
+                                 synchronous sweep loop re-ran it (the buffers then stay grown) */
 } csfs_b200_stats;
 
 /* --- lifetime ------------------------------------------------------------------------ */

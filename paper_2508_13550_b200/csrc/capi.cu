@@ -212,6 +212,7 @@ void fill_stats(csfs_b200_ctx* c, csfs_b200_stats* st) {
     st->src_leaves = c->shared ? st->tgt_leaves : S.ncl - count_internal(S);
     st->shared_tree = c->shared ? 1 : 0;
     st->n_ranks = 1;
+    st->traversal_fallback = c->lists.fallback ? 1 : 0;
 }
 
 // w_ready: optional event the weights' producer records (the host API copies them on

@@ -71,6 +71,7 @@ struct TreeView {
     // proxies: cluster c owns [c*npp, (c+1)*npp), index k1*np+k2 (interpolation.cpp:64-67)
     const double *qx, *qy, *qz;
     const double* qrad;  // per cluster: max chordal distance from the centre to its proxy points
+    const int* off_sphere;  // device flag: some particle is not a unit vector (guard everything)
 };
 
 struct DeviceTree {
@@ -94,6 +95,7 @@ struct DeviceTree {
     // proxies
     DevBuf<double> qx, qy, qz, qrad;
     DevBuf<double> qw;    // proxy weights (source side), ncl*npp
+    DevBuf<int> off_sphere;  // 1 flag: a particle with | |x|^2 - 1 | > 1e-12 (tree.cu k_face)
     DevBuf<double> qphi;  // proxy potentials (target side), ncl*npp*dim
 
     void reserve_clusters(int n_needed, cudaStream_t s);
@@ -119,6 +121,7 @@ struct Lists {
     long long n[4] = {0, 0, 0, 0};
     DevBuf<int2> front, front2;
     DevBuf<int> cnt;  // sweep counters of the host-free traversal
+    bool fallback = false;  // the last traversal overflowed a buffer and re-ran synchronously
 };
 
 // Work items for the unified evaluation kernel: one item per target leaf (PP+PC

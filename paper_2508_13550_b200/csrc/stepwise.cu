@@ -15,6 +15,7 @@
 // context's device trees in a level-major order (depth, then reference id), runs the same
 // kernels as the fused path, and hands results back in reference ids and input order.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 
@@ -107,6 +108,13 @@ void upload_tree(DeviceTree& T, const csfs_b200_tree_desc* d, const double* w_in
 
     // particles (tree order): SoA positions, face coordinates, permutation, weights
     const size_t nn = size_t(std::max<long long>(n, 1));
+    int off = 0;
+    for (long long t = 0; t < n && !off; ++t) {
+        const double* x = d->xyz + 3 * t;
+        off = !(std::fabs(x[0] * x[0] + x[1] * x[1] + x[2] * x[2] - 1.0) <= 1e-12);
+    }
+    T.off_sphere.grow(1);
+    CSFS_CK(cudaMemcpy(T.off_sphere.p, &off, sizeof(int), cudaMemcpyHostToDevice));
     for (DevBuf<double>* b : {&T.px, &T.py, &T.pz, &T.xi, &T.eta, &T.w}) b->grow(nn);
     for (DevBuf<int>* b : {&T.perm, &T.node}) b->grow(nn);
     std::vector<double> col(n);

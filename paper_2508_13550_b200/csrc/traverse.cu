@@ -507,7 +507,9 @@ void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, in
         return e ? std::atoll(e) : 0LL;
     }();
     const long long guess = guess_env > 0 ? guess_env : 16LL * (tgt.ncl + src.ncl) + 4096;
+    L.fallback = false;
     if (dual_traversal_async(T, S, tgt.depth_max() + src.depth_max(), mac, n0, seeds, guess, L, sc, s)) return;
+    L.fallback = true;
     for (int k = 0; k < 4; ++k) L.n[k] = 0;
     long long F = (long long)seeds.size();
     L.front.grow(std::max<long long>(F, 64));

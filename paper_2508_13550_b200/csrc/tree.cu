@@ -30,16 +30,21 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kLocalMinClusters = CSFS_LOCAL_MIN;  // frontier size from which levels split locally
 
+// Also flags points off the unit sphere (| |x|^2 - 1 | > 1e-12): the coincidence-guard
+// elision of the evaluation (traverse.cu needs_guard) assumes unit vectors, so a tree with
+// such points keeps the guard on every list entry (the reference's behaviour).
 __global__ void k_face(const double* __restrict__ xyz, long long n, int* fface, double* fxi,
-                       double* feta) {
+                       double* feta, int* off_sphere) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int f;
     double a, b;
-    face_project(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], f, a, b);
+    const double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    face_project(x, y, z, f, a, b);
     fface[i] = f;
     fxi[i] = a;
     feta[i] = b;
+    if (!(fabs(x * x + y * y + z * z - 1.0) <= 1e-12)) atomicOr(off_sphere, 1);
 }
 
 struct ClusterPtrs {
@@ -672,6 +677,7 @@ TreeView DeviceTree::view() const {
     v.rad = rad;
     v.qx = qx;
     v.qrad = qrad;
+    v.off_sphere = off_sphere;
     v.qy = qy;
     v.qz = qz;
     return v;
@@ -706,7 +712,9 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
     const int gp = ceil_div(n, kThreads);
 
     // ---- level 0: faces (cluster_tree.cpp:35-50) ------------------------------------------
-    k_face<<<gp, kThreads, 0, s>>>(xyz, n, sc.fface, sc.fxi, sc.feta);
+    t.off_sphere.grow(1);
+    CSFS_CK(cudaMemsetAsync(t.off_sphere.p, 0, sizeof(int), s));
+    k_face<<<gp, kThreads, 0, s>>>(xyz, n, sc.fface, sc.fxi, sc.feta, t.off_sphere);
     CSFS_LAUNCH_CHECK();
     {
         const int* fface = sc.fface;

@@ -128,3 +128,15 @@ def test_asymmetric_target_source_sizes(engine):
 def test_sal_parameters(engine, sal):
     x, w = blobs(20000, 12)
     check(engine, x, x, w, "sal", sal=sal, degree=8, mac=0.6, n0=64)
+
+
+@pytest.mark.parametrize("kernel", ["laplace", "sal", "biot_savart"])
+def test_points_off_the_unit_sphere(engine, kernel):
+    """Radii scattered in [0.98, 1.02]: the coincidence-guard elision assumes unit vectors, so
+    the engine keeps the guard on every entry (k_face flags the tree) and matches the
+    reference, which skips pairs with 1 - x.y < 1e-14 whatever their distance."""
+    rng = np.random.default_rng(11)
+    x = unit(rng.normal(size=(20000, 3))) * rng.uniform(0.98, 1.02, size=(20000, 1))
+    x[:50] = x[50:100] * (1.0 / np.einsum("ij,ij->i", x[50:100], x[50:100]))[:, None]  # x.y = 1 exactly-ish
+    w = rng.normal(size=20000)
+    check(engine, x, x, w, kernel, degree=6, mac=0.7, n0=64)

@@ -21,7 +21,7 @@ import json, sys
 import numpy as np
 sys.path.insert(0, sys.argv[1])
 from oracle import ref
-from paper_2508_13550_b200 import Engine, Kernel, ParticleSet, TraversalConfig
+from paper_2508_13550_b200 import Engine, Kernel, ParticleSet, SumStats, TraversalConfig
 from paper_2508_13550_b200.grids import cubed_sphere
 
 def sorted_pairs(a):
@@ -34,14 +34,16 @@ eng = Engine(0)
 cfg = TraversalConfig(mac=0.6, degree=6, n0=32)
 rt = ref.Tree(xyz, 6, 32)
 rl = ref.lists(rt, rt, 0.6, 32)
-out, same_lists = [], []
+out, same_lists, fallback = [], [], []
 for call in range(2):
-    g = eng.csfmm_sum(ParticleSet(xyz, w), ParticleSet(xyz, w), Kernel.parse("sal"), cfg).values
+    st = SumStats()
+    g = eng.csfmm_sum(ParticleSet(xyz, w), ParticleSet(xyz, w), Kernel.parse("sal"), cfg, st).values
+    fallback.append(st.traversal_fallback)
     gl = eng.lists_export()
     same_lists.append(all(np.array_equal(gl[k], sorted_pairs(rl[k])) for k in ("pp", "pc", "cp", "cc")))
     out.append(g)
 r, _ = ref.csfmm(xyz, xyz, w, "sal", mac=0.6, degree=6, n0=32)
-print(json.dumps({"lists": same_lists, "bitwise": bool(np.array_equal(out[0], out[1])),
+print(json.dumps({"lists": same_lists, "bitwise": bool(np.array_equal(out[0], out[1])), "fallback": fallback,
                   "rel_l2": float(np.sqrt(np.sum((out[1] - r) ** 2) / np.sum(r ** 2))),
                   "n_pp": int(len(rl["pp"]))}))
 """
@@ -58,5 +60,8 @@ def test_traversal_paths(guess):
     d = json.loads(res.stdout.strip().splitlines()[-1])
     assert d["n_pp"] > 64
     assert d["lists"] == [True, True]
+    # the tiny guess overflows on the first call only (the buffers stay grown); the default
+    # guess never falls back
+    assert d["fallback"] == ([1, 0] if guess != "0" else [0, 0])
     assert d["bitwise"]
     assert d["rel_l2"] < 1e-10
