@@ -56,11 +56,12 @@ __device__ __forceinline__ int classify(const TreeView& T, const TreeView& S, in
 // 1e-6 (chordal; the guard triggers below ~1.4e-7), either by the bounding spheres
 // (centre distance minus particle / proxy radii) or, for particle sets on one cube face,
 // by a gap of more than 1e-4 rad between their shrunk (xi, eta) boxes (the equiangular map
-// shrinks distances by at most a small constant factor).  Same cluster of the same tree:
-// always guarded.
+// shrinks distances by at most a small constant factor).  Same cluster of the same tree, or
+// a tree holding points off the unit sphere (k_face flags it): always guarded.
 __device__ __forceinline__ bool needs_guard(const TreeView& T, const TreeView& S, int t, bool t_prox, int s,
                                             bool s_prox) {
     if (T.px == S.px && t == s && !t_prox && !s_prox) return true;
+    if (*T.off_sphere || *S.off_sphere) return true;  // the bounds below assume |x| = 1
     const double dx = T.cx[t] - S.cx[s], dy = T.cy[t] - S.cy[s], dz = T.cz[t] - S.cz[s];
     const double R = sqrt(dx * dx + dy * dy + dz * dz);
     const double rt = t_prox ? T.qrad[t] : T.rad[t], rs = s_prox ? S.qrad[s] : S.rad[s];

@@ -1,17 +1,20 @@
 """GPU: the BASELINE.json configs at their FULL sizes against the reference's own
 csfmm_sum run on the host cores (oracle/_ref, all threads): potentials within the
-north_star bar (1e-10 relative L2), identical list sizes and tree statistics, and the
-FMM-vs-direct error equal to the reference's (direct sums on sampled targets, computed by
-the GPU all-pairs kernel, which itself matches the reference's direct_sum to 1e-12).
+north_star bar (1e-10 relative L2), the FMM-vs-direct error equal to the reference's
+(direct sums on sampled targets, computed by the GPU all-pairs kernel, which itself
+matches the reference's direct_sum to 1e-12), and the north_star's bit-exact structure:
+tree order (perm), topology in reference ids, the sorted PP/PC/CP/CC sets, geometry and
+proxy points within 1e-13, proxy weights within 1e-12 — at C2, C3, C5 and at each of the
+four RK4 stages of C4 (L9, positions advected with the GPU's own stage velocities).
 
-C1 is covered in full (including the tree/list dumps) by tests/test_gpu_parity.py and
-C4 (one RK4 step at L9) by tests/test_gpu_bve.py.  The reference takes ~1-2 minutes for
-C5 on a 16-core host."""
+C1 is covered in full by tests/test_gpu_parity.py.  The reference takes ~40 s for C5 on
+a 16-core host."""
 import numpy as np
 import pytest
 
 from oracle import ref
 from paper_2508_13550_b200 import Kernel, ParticleSet, SumStats, TraversalConfig, configs
+from test_gpu_parity import check_structure
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -35,6 +38,8 @@ def test_full_config_parity(engine, name):
     assert e < 1e-10
     assert (st.pp, st.pc, st.cp, st.cc) == tuple(int(v) for v in rst[5:9])
     assert (st.tgt_depth, st.tgt_clusters, st.tgt_leaves) == tuple(int(v) for v in rst[12:15])
+    # bit-exact structure: perm, topology (reference ids), the four list sets
+    check_structure(engine, wl.xyz, wl.degree, wl.n0, wl.mac, w=wl.weights)
     # FMM-vs-direct error: same as the reference's at the same degree and MAC
     rng = np.random.default_rng(7)
     idx = np.sort(rng.choice(wl.n, 4096, replace=False))
@@ -67,3 +72,36 @@ def test_beyond_baseline_size(engine):
           f"{st.t_total * 1e3:.1f} ms")
     assert e < 2e-9
     assert 3.5e6 < st.pp < 4.5e6
+
+
+def normalized(v):
+    return v / np.linalg.norm(v, axis=1, keepdims=True)
+
+
+def test_c4_rk4_stage_structure(engine):
+    """C4 at full size (L9), the four RK4 stages of bve_step (applications.cpp:378-412):
+    stage positions pos = normalized(x + h k) and vorticities from the GPU's own stage
+    velocities; at every stage the trees, lists and proxy weights are the reference's bit
+    for bit (stages 2-4 are advected: irregular leaves, PC entries) and the velocities agree
+    within 1e-10."""
+    wl = configs.make("c4")
+    cfg = TraversalConfig(mac=wl.mac, degree=wl.degree, n0=wl.n0)
+    k = Kernel.parse("biot_savart")
+    omega, dt = wl.meta["omega_per_day"], wl.meta["dt_days"]
+    x0, z0 = wl.xyz, wl.f
+    pos, zeta = x0, z0
+    for q, h in enumerate([0.5 * dt, 0.5 * dt, dt, None]):
+        w = zeta * wl.areas
+        st = SumStats()
+        p = ParticleSet(pos, w)
+        kq = engine.csfmm_sum(p, p, k, cfg, st).values.reshape(-1, 3)
+        check_structure(engine, pos, wl.degree, wl.n0, wl.mac, w=w)
+        r, rst = ref.csfmm(pos, pos, w, "biot_savart", mac=wl.mac, degree=wl.degree, n0=wl.n0)
+        e = rel_l2(kq.reshape(-1), r)
+        print(f"c4 stage {q + 1}: rel L2 {e:.2e}, lists {st.pp}/{st.pc}/{st.cp}/{st.cc}")
+        assert e < 1e-10
+        if q >= 1:
+            assert st.pc > 0  # advected: irregular leaves, PC interactions
+        if h is not None:
+            pos = normalized(x0 + h * kq)
+            zeta = z0 - 2.0 * omega * h * kq[:, 2]
