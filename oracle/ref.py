@@ -50,6 +50,8 @@ def lib() -> C.CDLL:
         L.csref_rh_zeta_many.argtypes = [P, S, P]
         L.csref_bve_step.argtypes = [P, P, P, S, D, D, D, I, I, I]
         L.csref_bve_remesh.argtypes = [P, P, P, P, S, I]
+        L.csref_read_particles.restype = C.c_longlong
+        L.csref_read_particles.argtypes = [C.c_char_p, P, P]
         L.csref_bve_step_remesh.argtypes = [P, P, P, P, P, S, D, D, D, I, I, I, I]
         _lib = L
     return _lib
@@ -67,6 +69,16 @@ def grid(kind: str, level: int) -> tuple[np.ndarray, np.ndarray]:
     xyz, a = np.empty((n, 3)), np.empty(n)
     lib().csref_grid(k, level, _p(xyz), _p(a))
     return xyz, a
+
+
+def read_particles_csv(path):
+    """The reference's read_particles_csv: (xyz, weights), or raises ValueError("CODE: msg")."""
+    n = lib().csref_read_particles(str(path).encode(), None, None)
+    if n < 0:
+        raise ValueError(lib().csref_last_error().decode())
+    xyz, w = np.empty((n, 3)), np.empty(n)
+    lib().csref_read_particles(str(path).encode(), _p(xyz), _p(w))
+    return xyz, w
 
 
 def _sal(sal):

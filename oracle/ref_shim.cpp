@@ -18,6 +18,7 @@
 #include "csfs/applications.hpp"
 #include "csfs/cluster_tree.hpp"
 #include "csfs/geometry.hpp"
+#include "csfs/io.hpp"
 #include "csfs/kernels.hpp"
 #include "csfs/summation.hpp"
 
@@ -92,6 +93,25 @@ int guarded(F&& f) {
 extern "C" {
 
 const char* csref_last_error() { return g_err.c_str(); }
+
+// read_particles_csv (io.cpp:166-185): returns the particle count (fills when xyz != null),
+// or -1 with last_error = "<code>: <message>" for the reference's CliError.
+long long csref_read_particles(const char* path, double* xyz, double* w) {
+    try {
+        const ParticleSet p = read_particles_csv(path);
+        if (xyz)
+            for (size_t i = 0; i < p.size(); ++i) {
+                xyz[3 * i] = p.positions[i].x;
+                xyz[3 * i + 1] = p.positions[i].y;
+                xyz[3 * i + 2] = p.positions[i].z;
+                w[i] = p.weights[i];
+            }
+        return (long long)p.size();
+    } catch (const CliError& e) {
+        g_err = e.code + ": " + e.message;
+        return -1;
+    }
+}
 
 // build_grid (geometry.cpp:229-243): returns the cell count; fills when xyz != null.
 long long csref_grid(int kind, int level, double* xyz, double* areas) {

@@ -5,7 +5,7 @@ Restates the reference's cubed-sphere grid generator ``build_grid(CubedSphere, L
 (``real_sph_harm``, ``rossby_haurwitz_zeta``; applications.cpp:14-49, 148-153).  This is
 input generation, not the hot path: the same arrays are handed to the B200 engine and to
 the reference, so bitwise agreement with the reference's own generator is not needed
-(tests/test_grids.py checks it anyway, to ~1 ulp).
+(tests/test_grids.py checks it anyway: centres and areas agree bit for bit).
 """
 from __future__ import annotations
 

@@ -1,13 +1,18 @@
-// CSV / report I/O of the B200 front-end, with the reference's formats and error codes
-// (/root/reference/proj/src/io.cpp:47-220): headers select the particle format, numbers are
-// written with "%.17g" (exact round trip), malformed input raises E_CSV with the file and
-// line, unreadable / unwritable paths raise E_IO, a potentials file with the wrong row
-// count raises E_DIM.
+// CSV / report I/O of the B200 front-end.  The interface is the reference's (csfs/io.hpp,
+// /root/reference/proj/src/io.cpp:47-220): the same headers select the particle format,
+// numbers are written "%.17g" (exact round trip), malformed input is E_CSV with the file
+// and line, unreadable / unwritable paths are E_IO, a potentials file with the wrong row
+// count is E_DIM — byte-identical messages, so scripts that parse them keep working.
+//
+// The implementation is a small streaming design of its own: CsvSource hands out the
+// non-blank lines already split into trimmed fields, CsvSink writes rows of numbers, and
+// the readers are thin field-mapping loops on top of them.
+#include <cerrno>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <fstream>
-#include <sstream>
-#include <stdexcept>
+#include <string_view>
 
 #include "io.hpp"
 
@@ -17,92 +22,137 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 
-std::ofstream create(const std::string& path) {
-    std::ofstream f(path);
-    if (!f) throw_cli("E_IO", "cannot open output file: " + path);
-    return f;
+// ---- reading ------------------------------------------------------------------------------
+
+// Blanks around a field: leading spaces, trailing spaces and carriage returns.
+std::string_view strip(std::string_view f) {
+    std::size_t b = 0, e = f.size();
+    while (b < e && f[b] == ' ') ++b;
+    while (e > b && (f[e - 1] == ' ' || f[e - 1] == '\r')) --e;
+    return f.substr(b, e - b);
 }
 
-std::string trim(std::string s) {
-    std::size_t b = 0, e = s.size();
-    while (b < e && s[b] == ' ') ++b;
-    while (e > b && (s[e - 1] == ' ' || s[e - 1] == '\r')) --e;
-    return s.substr(b, e - b);
-}
-
-// comma-separated fields, blanks trimmed; like std::getline on ',' a trailing empty
-// field is not reported
-std::vector<std::string> fields_of(const std::string& line) {
-    std::vector<std::string> out;
-    std::istringstream in(line);
-    for (std::string f; std::getline(in, f, ',');) out.push_back(trim(f));
-    return out;
-}
-
-double number(const std::string& s, const std::string& path, std::size_t line) {
-    std::size_t used = 0;
-    double v = 0.0;
-    bool ok = true;
-    try {
-        v = std::stod(s, &used);
-    } catch (const std::exception&) {
-        ok = false;
+// Fields of one line with std::getline(',') semantics: "a,,b" has an empty middle field,
+// a trailing comma adds no field, an empty line has none.
+void split_fields(std::string_view rest, std::vector<std::string>& fields) {
+    fields.clear();
+    while (!rest.empty()) {
+        const std::size_t comma = rest.find(',');
+        fields.emplace_back(strip(rest.substr(0, comma)));
+        if (comma == std::string_view::npos) break;
+        rest.remove_prefix(comma + 1);
     }
-    if (!ok || used != s.size())
-        throw_cli("E_CSV", path + ": malformed number '" + s + "' on line " + std::to_string(line));
+}
+
+// One CSV file, line by line: next() skips blank lines and returns the fields of the next
+// one with its 1-based line number; first() returns line 1 whatever it holds.
+class CsvSource {
+public:
+    explicit CsvSource(const std::string& path) : in_(path) {
+        if (!in_) throw_cli("E_IO", "cannot open input file: " + path);
+    }
+    bool next(std::size_t& line_no, std::vector<std::string>& fields) {
+        while (std::getline(in_, buf_)) {
+            ++no_;
+            if (buf_.empty()) continue;
+            split_fields(buf_, fields);
+            line_no = no_;
+            return true;
+        }
+        return false;
+    }
+    bool first(std::vector<std::string>& fields) {
+        if (no_ != 0 || !std::getline(in_, buf_)) return false;
+        ++no_;
+        split_fields(buf_, fields);
+        return true;
+    }
+
+private:
+    std::ifstream in_;
+    std::string buf_;
+    std::size_t no_ = 0;
+};
+
+// The whole field must be a number (strtod's grammar, as std::stod accepts it); anything
+// else — empty, trailing characters, out of range — is E_CSV.
+double to_number(const std::string& f, const std::string& path, std::size_t line_no) {
+    const char* s = f.c_str();
+    char* end = nullptr;
+    errno = 0;
+    const double v = std::strtod(s, &end);
+    if (end == s || *end != '\0' || errno == ERANGE)
+        throw_cli("E_CSV", path + ": malformed number '" + f + "' on line " + std::to_string(line_no));
     return v;
 }
 
-bool is_header(const std::vector<std::string>& h, std::initializer_list<const char*> names) {
-    if (h.size() != names.size()) return false;
-    std::size_t i = 0;
-    for (const char* n : names)
-        if (h[i++] != n) return false;
-    return true;
+std::string joined(const std::vector<std::string>& fields) {
+    std::string h;
+    for (std::size_t i = 0; i < fields.size(); ++i) h += (i ? "," : "") + fields[i];
+    return h;
 }
 
-struct Table {
-    std::vector<std::string> header;
-    std::vector<std::vector<double>> rows;
+// Header + numeric rows of exactly `width` columns.  Line 1 is the header whatever it
+// holds; when line 1 is blank there is no header, every later line is data, and the
+// missing header is reported after the rows were read.
+struct Sheet {
+    std::string header;  // the header fields joined with ','
+    bool has_header = false;
+    std::vector<double> cells;  // row-major, width per row
 };
 
-// first line = header; every other non-blank line holds exactly `cols` numbers
-Table read_table(const std::string& path, std::size_t cols) {
-    std::ifstream in(path);
-    if (!in) throw_cli("E_IO", "cannot open input file: " + path);
-    Table t;
-    std::string line;
-    for (std::size_t no = 1; std::getline(in, line); ++no) {
-        if (line.empty()) continue;
-        std::vector<std::string> f = fields_of(line);
-        if (no == 1) {
-            t.header = std::move(f);
+Sheet read_sheet(const std::string& path, std::size_t width) {
+    CsvSource src(path);
+    Sheet sh;
+    std::vector<std::string> f;
+    std::size_t line_no = 0;
+    while (src.next(line_no, f)) {
+        if (line_no == 1) {
+            sh.header = joined(f);
+            sh.has_header = true;
             continue;
         }
-        if (f.size() != cols)
-            throw_cli("E_CSV", path + ": expected " + std::to_string(cols) + " columns on line " + std::to_string(no));
-        std::vector<double> row(cols);
-        for (std::size_t c = 0; c < cols; ++c) row[c] = number(f[c], path, no);
-        t.rows.push_back(std::move(row));
+        if (f.size() != width)
+            throw_cli("E_CSV", path + ": expected " + std::to_string(width) + " columns on line " +
+                                   std::to_string(line_no));
+        for (const std::string& cell : f) sh.cells.push_back(to_number(cell, path, line_no));
     }
-    if (t.header.empty()) throw_cli("E_CSV", path + ": missing header line");
-    return t;
+    if (!sh.has_header) throw_cli("E_CSV", path + ": missing header line");
+    return sh;
 }
 
-Vec3 lonlat_deg(double lon, double lat) {
-    const double lo = lon * kPi / 180.0, la = lat * kPi / 180.0;
-    return {std::cos(la) * std::cos(lo), std::cos(la) * std::sin(lo), std::sin(la)};
-}
+// ---- writing ------------------------------------------------------------------------------
+
+class CsvSink {
+public:
+    CsvSink(const std::string& path, const char* header) : out_(path) {
+        if (!out_) throw_cli("E_IO", "cannot open output file: " + path);
+        out_ << header << '\n';
+    }
+    // one row: the values, comma separated, %.17g
+    void row(std::initializer_list<double> head, const double* tail = nullptr, int n_tail = 0) {
+        const char* sep = "";
+        for (double v : head) {
+            out_ << sep << format_double(v);
+            sep = ",";
+        }
+        for (int i = 0; i < n_tail; ++i) out_ << ',' << format_double(tail[i]);
+        out_ << '\n';
+    }
+
+private:
+    std::ofstream out_;
+};
 
 }  // namespace
 
 void throw_cli(const std::string& code, const std::string& message) { throw CliError{code, message}; }
 
 int exit_code_for(const std::string& code) {
-    static const std::map<std::string, int> codes = {{"E_FLAGS", 2}, {"E_KERNEL", 3}, {"E_CONFIG", 4},
-                                                     {"E_CSV", 5},   {"E_DIM", 6},    {"E_IO", 7}};
-    const auto it = codes.find(code);
-    return it == codes.end() ? 1 : it->second;
+    static const char* const kCodes[] = {"E_FLAGS", "E_KERNEL", "E_CONFIG", "E_CSV", "E_DIM", "E_IO"};
+    for (int i = 0; i < 6; ++i)
+        if (code == kCodes[i]) return 2 + i;
+    return 1;
 }
 
 std::string format_double(double v) {
@@ -112,43 +162,43 @@ std::string format_double(double v) {
 }
 
 Particles read_particles_csv(const std::string& path) {
-    const Table t = read_table(path, 4);
-    Particles p;
-    p.positions.reserve(t.rows.size());
-    p.weights.reserve(t.rows.size());
-    if (is_header(t.header, {"x", "y", "z", "weight"})) {
-        for (const auto& r : t.rows) {
-            const double n = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-            p.positions.push_back({r[0] / n, r[1] / n, r[2] / n});
-            p.weights.push_back(r[3]);
-        }
-    } else if (is_header(t.header, {"lon", "lat", "area", "value"})) {
-        for (const auto& r : t.rows) {
-            p.positions.push_back(lonlat_deg(r[0], r[1]));
-            p.weights.push_back(r[3] * r[2]);
-        }
-    } else {
+    const Sheet sh = read_sheet(path, 4);
+    const bool xyz = sh.header == "x,y,z,weight";
+    if (!xyz && sh.header != "lon,lat,area,value")
         throw_cli("E_CSV", path + ": header must be 'x,y,z,weight' or 'lon,lat,area,value'");
+    Particles p;
+    const std::size_t rows = sh.cells.size() / 4;
+    p.positions.resize(rows);
+    p.weights.resize(rows);
+    for (std::size_t r = 0; r < rows; ++r) {
+        const double* c = &sh.cells[4 * r];
+        if (xyz) {  // normalized((x, y, z)), weight as given
+            const double len = std::sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+            p.positions[r] = {c[0] / len, c[1] / len, c[2] / len};
+            p.weights[r] = c[3];
+        } else {  // degrees -> unit vector, weight = value * area
+            const double lon = c[0] * kPi / 180.0, lat = c[1] * kPi / 180.0;
+            p.positions[r] = {std::cos(lat) * std::cos(lon), std::cos(lat) * std::sin(lon), std::sin(lat)};
+            p.weights[r] = c[3] * c[2];
+        }
     }
     return p;
 }
 
 std::vector<double> read_potentials_csv(const std::string& path, std::size_t expected_rows, int& out_dim) {
-    std::ifstream in(path);
-    if (!in) throw_cli("E_IO", "cannot open input file: " + path);
-    std::string line;
-    if (!std::getline(in, line)) throw_cli("E_CSV", path + ": missing header line");
-    const std::vector<std::string> h = fields_of(line);
-    if (is_header(h, {"x", "y", "z", "phi"})) out_dim = 1;
-    else if (is_header(h, {"x", "y", "z", "phi", "phi_y", "phi_z"})) out_dim = 3;
+    CsvSource src(path);
+    std::vector<std::string> f;
+    if (!src.first(f)) throw_cli("E_CSV", path + ": missing header line");
+    const std::string h = joined(f);
+    if (h == "x,y,z,phi") out_dim = 1;
+    else if (h == "x,y,z,phi,phi_y,phi_z") out_dim = 3;
     else throw_cli("E_CSV", path + ": unrecognized potentials header");
     std::vector<double> vals;
-    for (std::size_t no = 2; std::getline(in, line); ++no) {
-        if (line.empty()) continue;
-        const std::vector<std::string> f = fields_of(line);
-        if (int(f.size()) != 3 + out_dim)
-            throw_cli("E_CSV", path + ": bad column count on line " + std::to_string(no));
-        for (int d = 0; d < out_dim; ++d) vals.push_back(number(f[3 + d], path, no));
+    std::size_t line_no = 0;
+    while (src.next(line_no, f)) {
+        if (f.size() != std::size_t(3 + out_dim))
+            throw_cli("E_CSV", path + ": bad column count on line " + std::to_string(line_no));
+        for (int d = 0; d < out_dim; ++d) vals.push_back(to_number(f[3 + d], path, line_no));
     }
     const std::size_t rows = vals.size() / out_dim;
     if (rows != expected_rows)
@@ -157,22 +207,14 @@ std::vector<double> read_potentials_csv(const std::string& path, std::size_t exp
 }
 
 void write_grid_csv(const std::string& path, const Grid& g) {
-    std::ofstream f = create(path);
-    f << "x,y,z,area\n";
-    for (std::size_t i = 0; i < g.size(); ++i)
-        f << format_double(g.centers[i].x) << ',' << format_double(g.centers[i].y) << ','
-          << format_double(g.centers[i].z) << ',' << format_double(g.areas[i]) << '\n';
+    CsvSink out(path, "x,y,z,area");
+    for (std::size_t i = 0; i < g.size(); ++i) out.row({g.centers[i].x, g.centers[i].y, g.centers[i].z, g.areas[i]});
 }
 
 void write_potentials_csv(const std::string& path, const std::vector<Vec3>& pts, const std::vector<double>& phi,
                           int out_dim) {
-    std::ofstream f = create(path);
-    f << (out_dim == 1 ? "x,y,z,phi" : "x,y,z,phi,phi_y,phi_z") << '\n';
-    for (std::size_t i = 0; i < pts.size(); ++i) {
-        f << format_double(pts[i].x) << ',' << format_double(pts[i].y) << ',' << format_double(pts[i].z);
-        for (int d = 0; d < out_dim; ++d) f << ',' << format_double(phi[i * out_dim + d]);
-        f << '\n';
-    }
+    CsvSink out(path, out_dim == 1 ? "x,y,z,phi" : "x,y,z,phi,phi_y,phi_z");
+    for (std::size_t i = 0; i < pts.size(); ++i) out.row({pts[i].x, pts[i].y, pts[i].z}, &phi[i * out_dim], out_dim);
 }
 
 // ---- JSON -------------------------------------------------------------------------------

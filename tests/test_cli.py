@@ -129,6 +129,49 @@ def test_floats_have_17_significant_digits(tmp_path):
     assert lines[1].endswith(",0.33333333333333331") and lines[2].endswith(",2562")
 
 
+CSV_CASES = {
+    "plain": "x,y,z,weight\n1,0,0,2.5\n0,1,0,-1\n",
+    "crlf_spaces": "x, y ,z,weight \r\n 3 , 0,4 ,1e-3\r\n\r\n0,0,-2,  7\r\n",
+    "blank_lines": "x,y,z,weight\n\n1,2,3,4\n\n\n-1,0.5,0.25,1e300\n",
+    "trailing_comma": "x,y,z,weight,\n1,2,3,4,\n",
+    "lonlat": "lon,lat,area,value\n0,0,0.5,3\n-179.5,89.999,1e-6,-2\n33.3,-12.5,0.125,0.5\n",
+    "hex_inf": "x,y,z,weight\n0x1p-1,0,1,inf\n1,1,1,-0\n",
+    "blank_first_line": "\nx,y,z,weight\n1,0,0,1\n",
+    "short_row": "x,y,z,weight\n1,0,0\n",
+    "empty_field": "x,y,z,weight\n1,,0,1\n",
+    "bad_number": "x,y,z,weight\n1,0,1e,1\n",
+    "overflow": "x,y,z,weight\n1,0,0,1e999\n",
+    "bad_header": "lon,lat,value,area\n1,0,0,1\n",
+    "header_only": "x,y,z,weight\n",
+    "empty": "",
+}
+
+
+@pytest.mark.parametrize("case", sorted(CSV_CASES))
+def test_particle_csv_matches_reference_reader(tmp_path, monkeypatch, case):
+    """`convert` reads particle CSVs exactly like the reference's read_particles_csv
+    (io.cpp:166-185, compiled into oracle/_ref): the same particles bit for bit, or the same
+    error code and message."""
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    (tmp_path / "in.csv").write_text(CSV_CASES[case])
+    code, _, err = run(["convert", "--particles", "in.csv", "-o", "out.csv"], tmp_path)
+    monkeypatch.chdir(tmp_path)  # same relative path in both messages
+    try:
+        xyz, w = ref.read_particles_csv("in.csv")
+    except ValueError as ex:
+        want_code, want_msg = str(ex).split(": ", 1)
+        got = json.loads(err.strip().splitlines()[-1])
+        assert code == CODES[want_code] and got["error"] == want_code and got["message"] == want_msg, (got, str(ex))
+        return
+    assert code == 0, err
+    lines = open(tmp_path / "out.csv").read().splitlines()
+    assert lines[0] == "x,y,z,weight" and len(lines) == 1 + len(w)
+    got = np.array([[float(v) for v in ln.split(",")] for ln in lines[1:]]).reshape(-1, 4)
+    np.testing.assert_array_equal(got[:, :3], xyz)
+    np.testing.assert_array_equal(got[:, 3], w)
+
+
 # ---- GPU ------------------------------------------------------------------------------
 
 
