@@ -10,6 +10,8 @@
 // coefficient (fixed order; roundoff-level difference from the reference's serial sum,
 // within the 1e-12 proxy-weight bar); L2L is done separably.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "engine.hpp"
 #include "fastmath.cuh"
@@ -84,6 +86,78 @@ __global__ void __launch_bounds__(kPassThreads)
     for (int q = 0; q < kOut; ++q) {
         const int o = threadIdx.x + q * kPassThreads;
         if (o < npp) qw[(long long)c * npp + o] = (acc[q][0] + acc[q][1]) + (acc[q][2] + acc[q][3]);
+    }
+}
+
+// The same leaf P2M on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64): per leaf the
+// proxy weights are the GEMM  pw = (w Lx)^T Ly  over its particles, (np x m) (m x np),
+// padded to 8 x 8 output tiles (np <= 8: one tile; np <= 16: 2 x 2, one warp each), K in
+// steps of 4 particles.  The bases are staged per 128-particle chunk exactly as above
+// (zero-padded to the tile edge); each lane feeds one A and one B element per MMA.
+// Products are accumulated in the MMA's fused order (roundoff-level difference).
+// Selected with CSFS_B200_P2M=dmma — the A/B of DESIGN.md §3 (profiles/r02_p2m_dmma_vs_fma).
+template <int NP>
+__global__ void __launch_bounds__(kPassThreads)
+    k_p2m_dmma(TreeView t, Cheb cheb, const double* __restrict__ w, double* __restrict__ qw, int mode,
+               Own own) {
+    static_assert(NP > 0 && NP <= 16, "tile-padded degrees only");
+    constexpr int NPAD = NP <= 8 ? 8 : 16;
+    constexpr int TILES = NPAD / 8;  // per axis
+    // row stride: a fragment load touches 4 particle rows x 8 coefficients; rows 24 doubles
+    // apart fall in alternate bank halves (2 wavefronts, the minimum for 32 doubles)
+    constexpr int LDW = NPAD == 16 ? 24 : 8;
+    __shared__ double WL[kP2mChunk * LDW];  // [particle][k1], zero-padded
+    __shared__ double LY[kP2mChunk * LDW];  // [particle][k2]
+    const int c = blockIdx.x;
+    if (t.nchild[c] > 0 || !selected(t, c, mode, own)) return;
+    const int b = t.begin[c], e = t.end[c];
+    const double x0 = t.xi0[c], x1 = t.xi1[c], e0 = t.eta0[c], e1 = t.eta1[c];
+    const double xm = __dmul_rn(0.5, __dadd_rn(x0, x1)), xh = __dmul_rn(0.5, __dsub_rn(x1, x0));
+    const double em = __dmul_rn(0.5, __dadd_rn(e0, e1)), eh = __dmul_rn(0.5, __dsub_rn(e1, e0));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool mma_warp = warp < TILES * TILES;
+    const int r0 = (warp / TILES) * 8, c0 = (warp % TILES) * 8;  // output tile origin (k1, k2)
+    const int arow = lane >> 2, acol = lane & 3;                 // fragment coordinates
+    // C/D fragments (row arow, cols 2 acol, +1): 4 independent accumulator chains over the
+    // K steps (the MMA latency, not its issue, bounds one chain), summed in fixed order
+    double d0[4] = {0.0, 0.0, 0.0, 0.0}, d1[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int base = b; base < e; base += kP2mChunk) {
+        const int m = min(kP2mChunk, e - base);
+        for (int j = threadIdx.x; j < kP2mChunk; j += kPassThreads) {
+            double lx[NP], ly[NP];
+            double wt = 0.0;
+            if (j < m) {
+                bary1d_fast<NP>(cheb, ref_coord(t.xi[base + j], xm, xh), lx);
+                bary1d_fast<NP>(cheb, ref_coord(t.eta[base + j], em, eh), ly);
+                wt = w[base + j];
+            }
+#pragma unroll
+            for (int k = 0; k < NPAD; ++k) {
+                WL[j * LDW + k] = (j < m && k < NP) ? __dmul_rn(wt, lx[k < NP ? k : 0]) : 0.0;
+                LY[j * LDW + k] = (j < m && k < NP) ? ly[k < NP ? k : 0] : 0.0;
+            }
+        }
+        __syncthreads();
+        if (mma_warp) {
+            const int steps = (m + 15) >> 4;  // 4 K-steps of 4 particles per iteration (zero-padded rows)
+            for (int s = 0; s < steps; ++s) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int tp = 16 * s + 4 * u + acol;  // particle of this lane's A row / B column
+                    const double a = WL[tp * LDW + r0 + arow];
+                    const double bb = LY[tp * LDW + c0 + arow];
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                 : "+d"(d0[u]), "+d"(d1[u]) : "d"(a), "d"(bb));
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (mma_warp) {
+        const int k1 = r0 + arow, k2 = c0 + 2 * acol;
+        const double s0 = (d0[0] + d0[1]) + (d0[2] + d0[3]), s1 = (d1[0] + d1[1]) + (d1[2] + d1[3]);
+        if (k1 < NP && k2 < NP) qw[(long long)c * NP * NP + k1 * NP + k2] = s0;
+        if (k1 < NP && k2 + 1 < NP) qw[(long long)c * NP * NP + k1 * NP + k2 + 1] = s1;
     }
 }
 
@@ -266,10 +340,15 @@ void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s, int mode, Ow
     const size_t sm_p2m = size_t(2) * kP2mChunk * np * sizeof(double);
     const int n_p2m = mode == 2 ? src.level_count[0] : src.ncl;  // depth 0 = ids 0..5
     auto p2m = [&](auto kern) { kern<<<n_p2m, kPassThreads, sm_p2m, s>>>(v, cheb, src.w, src.qw, mode, own); };
+    auto p2m_tc = [&](auto kern) { kern<<<n_p2m, kPassThreads, 0, s>>>(v, cheb, src.w, src.qw, mode, own); };
+    static const bool dmma = [] {
+        const char* e = std::getenv("CSFS_B200_P2M");
+        return e && std::string(e) == "dmma";
+    }();
     switch (np) {
-        case 7: p2m(k_p2m<7>); break;
-        case 9: p2m(k_p2m<9>); break;
-        case 11: p2m(k_p2m<11>); break;
+        case 7: dmma ? p2m_tc(k_p2m_dmma<7>) : p2m(k_p2m<7>); break;
+        case 9: dmma ? p2m_tc(k_p2m_dmma<9>) : p2m(k_p2m<9>); break;
+        case 11: dmma ? p2m_tc(k_p2m_dmma<11>) : p2m(k_p2m<11>); break;
         default: p2m(k_p2m<0>);
     }
     CSFS_LAUNCH_CHECK();
