@@ -251,6 +251,14 @@ CSFS_B200_API int csfs_b200_create_emulated(csfs_b200_ctx** out, int device, int
 CSFS_B200_API int csfs_b200_group_info(const csfs_b200_ctx* ctx, int* nranks, int* rank, int* devices,
                                        long long* t_ranges, long long* s_ranges);
 
+/* Per-rank phases of the last partitioned call with stats, for the ranks this process
+ * runs (Multi / Emulated: all, in rank order; Rank: this one): 6 values each — plan,
+ * upward + pack, interact, downward, finish (ms, CUDA events on the rank's stream) and the
+ * bytes the rank broadcasts in the two all-gathers.  *n = values available; min(cap, *n)
+ * are written.  In Emulated mode the phases ran alone on the device, so they are the
+ * per-rank cost of an N-GPU step without the exchanges (tools/scaling_emulation.py). */
+CSFS_B200_API int csfs_b200_group_phases(const csfs_b200_ctx* ctx, double* out, int cap, int* n);
+
 /* TreeStats::leaf_size_histogram (cluster_tree.cpp:149-161) of the last call's target
  * (which 0) or source (1) tree: bucket i counts the leaves with i particles (empty face
  * roots included).  *len = max leaf size + 1; min(cap, *len) buckets are written. */

@@ -70,6 +70,9 @@ struct csfs_b200_ctx {
     std::vector<long long> xq_off;     // per rank: first cluster of its segment in xidx (+ end)
     std::vector<long long> t_range, s_range;  // per rank: owned tree-order [b, e) x 2
     double t_exchange = 0.0;           // last call: seconds in the two exchanges (rank 0)
+    // last call, per rank of this process: plan, upward + pack, interact, downward, finish (ms)
+    // and the bytes the rank broadcasts in the two exchanges
+    std::vector<double> rank_phases;
 };
 
 namespace csfs_b200 {

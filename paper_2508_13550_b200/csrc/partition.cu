@@ -335,6 +335,18 @@ void group_stats(Ctx* c, const std::vector<Ctx*>& ranks, const std::vector<unsig
     }
     st->t_total = tmax;
     st->evals_executed = ex;
+    c->rank_phases.clear();
+    for (size_t r = 0; r < ranks.size(); ++r) {
+        const Ctx* q = ranks[r];
+        const cudaEvent_t* e = q->ev;
+        const int rk = q->rank;
+        const DeviceTree& S = q->shared ? q->ttree : q->stree;
+        const double bytes = 8.0 * double(q->xq_off[rk + 1] - q->xq_off[rk]) * S.npp +
+                             8.0 * double(q->t_range[2 * rk + 1] - q->t_range[2 * rk]) * q->dim;
+        for (double v : {double(ev_ms(e[0], e[1])), double(ev_ms(e[1], e[2])), double(ev_ms(e[3], e[4])),
+                         double(ev_ms(e[4], e[5])), double(ev_ms(e[6], e[7])), bytes})
+            c->rank_phases.push_back(v);
+    }
     st->n_ranks = c->nranks;
     st->symmetric_pairs = c->items.mutual ? c->items.n_mutual : 0;
 }
@@ -497,6 +509,13 @@ int csfs_b200_create_emulated(csfs_b200_ctx** out, int device, int nranks) {
     std::unique_ptr<Ctx> root = std::move(cs[0]);
     for (int i = 1; i < nranks; ++i) root->peers.push_back(std::move(cs[i]));
     *out = root.release();
+    return CSFS_B200_OK;
+}
+
+int csfs_b200_group_phases(const csfs_b200_ctx* c, double* out, int cap, int* n) {
+    if (!c) return CSFS_B200_INVALID_ARGUMENT;
+    if (n) *n = int(c->rank_phases.size());
+    for (int i = 0; i < std::min<int>(cap, int(c->rank_phases.size())); ++i) out[i] = c->rank_phases[i];
     return CSFS_B200_OK;
 }
 

@@ -177,6 +177,7 @@ def lib() -> C.CDLL:
         L.csfs_b200_nccl_unique_id.argtypes = [C.c_char_p]
         L.csfs_b200_group_info.argtypes = [P, C.POINTER(I), C.POINTER(I), P, P, P]
         L.csfs_b200_leaf_histogram.argtypes = [P, I, P, I, C.POINTER(I)]
+        L.csfs_b200_group_phases.argtypes = [P, P, I, C.POINTER(I)]
         _lib = L
     return _lib
 
@@ -274,6 +275,15 @@ class Engine:
             info["target_ranges"] = tr.reshape(-1, 2).tolist()
             info["source_ranges"] = sr.reshape(-1, 2).tolist()
         return info
+
+    def group_phases(self) -> list[dict]:
+        """Per-rank phases of the last partitioned call made with stats (csfs_b200_group_phases)."""
+        n = C.c_int()
+        self._check(self._lib.csfs_b200_group_phases(self._h, None, 0, C.byref(n)))
+        v = np.empty(n.value)
+        self._check(self._lib.csfs_b200_group_phases(self._h, _ptr(v), n.value, C.byref(n)))
+        keys = ("plan_ms", "upward_ms", "interact_ms", "downward_ms", "finish_ms", "exchange_bytes")
+        return [dict(zip(keys, v[i:i + 6].tolist())) for i in range(0, v.size, 6)]
 
     def leaf_histogram(self, which: int) -> list[int]:
         """TreeStats::leaf_size_histogram of the last call's target (0) / source (1) tree."""

@@ -1,75 +1,71 @@
-"""Per-rank cost of the target-partitioned multi-GPU step, emulated on ONE GPU.
+"""Per-rank cost of the target-partitioned multi-GPU csfmm, emulated on ONE GPU.
 
-For world W in 1, 2, 4, 8 every rank's device work is run one rank after another and timed
-with CUDA events: the replicated part (part_plan: trees, lists, items, symmetric pairs),
-the rank's owned upward pass, its owned evaluation + downward pass, and the final scatter.
-Nothing here waits on another rank (SURVEY/B200_PROFILING: no cross-rank spin on one GPU);
-the two all-reduces (proxy weights, tree-order potentials) are not run — their volume is
-reported instead.  The projected step time at W GPUs is max over ranks of the rank's own
-work; the real multi-GPU run adds the all-reduces over NVLink.
+csfs_b200_create_emulated(device, W) runs the W ranks of the library's own partitioned
+path (partition.cu: replicated plan, owned upward pass, owner-packed proxy-weight
+exchange, owned evaluation + downward pass, potential exchange, scatter) phase by phase on
+one device, the two all-gathers done as device copies.  Every rank's phases run alone on
+the GPU and are timed with CUDA events (csfs_b200_group_phases), so nothing waits on
+another rank (B200_PROFILING: no cross-rank spin on one GPU).  The projected step at W
+GPUs is the slowest rank's own work plus its all-gather time at NVLink rate: the ranks'
+broadcast bytes / NVLINK_GBS (the NCCL exchanges themselves run only on a multi-GPU box).
+The result is bitwise the same for every W (checked here against W = 1).
 
-    python tools/scaling_emulation.py [config]
+    python tools/scaling_emulation.py [config] [out.json]
 """
 import json
 import sys
 
-import torch
-
-REPS = 3  # each rank's phases timed REPS times, min kept (one-off clock dips excluded)
+import numpy as np
 
 sys.path.insert(0, ".")
-from paper_2508_13550_b200 import Engine, Kernel, TraversalConfig, configs  # noqa: E402
-from paper_2508_13550_b200.distributed import plan_partition  # noqa: E402
+from paper_2508_13550_b200 import Engine, Kernel, ParticleSet, SumStats, TraversalConfig, configs  # noqa: E402
 
-
-def timed(fn):
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1)
+NVLINK_GBS = 450.0  # per-GPU all-gather bus bandwidth assumed for the projection (NVLink 5: 900 GB/s/direction)
+REPS = 3
 
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+    out = sys.argv[2] if len(sys.argv) > 2 else None
     wl = configs.make(name)
-    dev = torch.device("cuda", 0)
-    eng = Engine(0)
-    xyz = torch.from_numpy(wl.xyz).to(dev)
-    w = torch.from_numpy(wl.weights).to(dev)
     k = Kernel.parse(wl.kernel)
     cfg = TraversalConfig(mac=wl.mac, degree=wl.degree, n0=wl.n0)
-    s = torch.cuda.current_stream().cuda_stream
-    out = torch.empty(wl.n * k.out_dim(), dtype=torch.float64, device=dev)
-
-    def plan():
-        eng.part_plan(xyz.data_ptr(), wl.n, xyz.data_ptr(), w.data_ptr(), wl.n, k, cfg, s)
-
-    for _ in range(2):
-        plan()
-    t_plan = min(timed(plan) for _ in range(3))
-    n_pw, n_phi = eng.part_sizes()
-    pw = torch.zeros(n_pw, dtype=torch.float64, device=dev)
-    phi = torch.zeros(n_phi, dtype=torch.float64, device=dev)
-    res = {"config": name, "n": wl.n, "part_plan_ms": t_plan, "allreduce_bytes": 8 * (n_pw + n_phi), "worlds": []}
+    p = ParticleSet(wl.xyz, wl.weights)
+    res = {"config": name, "n": wl.n, "nvlink_gbs_assumed": NVLINK_GBS, "worlds": []}
+    base = None
     for world in (1, 2, 4, 8):
-        ranks = []
-        for r in range(world):
-            p = plan_partition(eng, r, world)
-            t_up = min(timed(lambda: eng.part_upward(*p.source_range, pw.data_ptr())) for _ in range(REPS))
-            t_ev = min(timed(lambda: eng.part_eval(*p.target_range, pw.data_ptr(), phi.data_ptr()))
-                       for _ in range(REPS))
-            t_fin = min(timed(lambda: eng.part_finish(phi.data_ptr(), out.data_ptr())) for _ in range(REPS))
-            ranks.append({"rank": r, "upward_ms": t_up, "eval_ms": t_ev, "finish_ms": t_fin,
-                          "total_ms": t_plan + t_up + t_ev + t_fin, "cost_share": p.target_cost_share})
-        step = max(x["total_ms"] for x in ranks)
-        res["worlds"].append({"world": world, "step_ms_max_rank": step, "pts_per_s": wl.n / (step * 1e-3),
-                              "ranks": ranks})
-        print(json.dumps({"world": world, "step_ms": step, "pts_per_s": wl.n / (step * 1e-3),
-                          "eval_ms": [round(x["eval_ms"], 2) for x in ranks]}), flush=True)
-    print(json.dumps(res))
+        g = Engine.emulated(0, world)
+        best = None
+        for _ in range(REPS + 1):
+            st = SumStats()
+            phi = g.csfmm_sum(p, p, k, cfg, st).values.copy()
+            ph = g.group_phases()
+            tot = [r["plan_ms"] + r["upward_ms"] + r["interact_ms"] + r["downward_ms"] + r["finish_ms"] for r in ph]
+            if best is None or max(tot) < best[0]:
+                best = (max(tot), ph, tot, st.evals_executed)
+        if base is None:
+            base = phi
+        bitwise = bool(np.array_equal(phi, base))
+        _, ph, tot, ex = best
+        # all-gather time: every rank receives all other ranks' segments; at the bus rate
+        # the step pays (total bytes - own) / bandwidth
+        total_bytes = sum(r["exchange_bytes"] for r in ph)
+        exch_ms = [(total_bytes - r["exchange_bytes"]) / (NVLINK_GBS * 1e9) * 1e3 if world > 1 else 0.0 for r in ph]
+        step = max(t + e for t, e in zip(tot, exch_ms))
+        rec = {"world": world, "step_ms_projected": step, "pts_per_s_projected": wl.n / (step * 1e-3),
+               "bitwise_equal_to_w1": bitwise, "evals_executed_all_ranks": ex,
+               "plan_ms_max": max(r["plan_ms"] for r in ph),
+               "interact_ms_max": max(r["interact_ms"] for r in ph),
+               "interact_ms_min": min(r["interact_ms"] for r in ph),
+               "exchange_ms_projected_max": max(exch_ms), "ranks": ph}
+        res["worlds"].append(rec)
+        print(json.dumps({kk: v for kk, v in rec.items() if kk != "ranks"}), flush=True)
+        g.close()
+    w1 = res["worlds"][0]["step_ms_projected"]
+    for r in res["worlds"]:
+        r["efficiency_vs_w1"] = w1 / (r["step_ms_projected"] * r["world"])
+    if out:
+        json.dump(res, open(out, "w"), indent=1)
 
 
 if __name__ == "__main__":
