@@ -101,9 +101,16 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
     for (;;) {
         if (tid == 0) item_sh = atomicAdd(P.counter, 1);
         __syncthreads();
-        const int it = item_sh;
+        const int q = item_sh;
         __syncthreads();
-        if (it >= P.n_items) break;
+        if (q >= P.n_items) break;
+#ifndef CSFS_ITEM_ORDER_REVERSED
+#define CSFS_ITEM_ORDER_REVERSED 1
+#endif
+        // the queue hands out the items back to front: cluster items (CP/CC, the largest,
+        // up to ~1.3M evaluations each at C5) first, the uniform leaf items last, so the
+        // kernel's tail is made of short items (longest-first scheduling)
+        const int it = CSFS_ITEM_ORDER_REVERSED ? P.n_items - 1 - q : q;
         if (P.anchor) {
             const int a = P.anchor[it];
             if (a >= 0 && (a < P.own_b || a >= P.own_e)) continue;  // another rank's target
