@@ -72,6 +72,7 @@ typedef struct {
     double t_exchange;        /* seconds in the two NCCL all-gathers (rank 0; 0 on one GPU) */
     int traversal_fallback;   /* 1: a host-free traversal sweep overflowed its buffers and the
                                  synchronous sweep loop re-ran it (the buffers then stay grown) */
+    uint64_t symmetric_partials; /* doubles in the symmetric pairs' partial-sum buffer (64-bit offsets) */
 } csfs_b200_stats;
 
 /* --- lifetime ------------------------------------------------------------------------ */

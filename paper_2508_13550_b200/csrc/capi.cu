@@ -213,6 +213,7 @@ void fill_stats(csfs_b200_ctx* c, csfs_b200_stats* st) {
     st->shared_tree = c->shared ? 1 : 0;
     st->n_ranks = 1;
     st->traversal_fallback = c->lists.fallback ? 1 : 0;
+    st->symmetric_partials = c->items.mutual ? (uint64_t)c->items.n_partial : 0;
 }
 
 // w_ready: optional event the weights' producer records (the host API copies them on

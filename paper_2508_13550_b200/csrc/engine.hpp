@@ -107,6 +107,7 @@ struct DeviceTree {
 struct Scratch {
     DevBuf<int> tiles;      // scan tile totals
     DevBuf<int> grand;      // scan grand totals (device)
+    DevBuf<long long> tiles64, grand64;  // the same for 64-bit counters (partial offsets)
     DevBuf<int> segP, segE, kid, koff;  // per frontier cluster x 4
     DevBuf<unsigned long long> qbnd;    // per frontier cluster x 16: quadrant bounds (local levels)
     DevBuf<int> counters;   // misc device counters

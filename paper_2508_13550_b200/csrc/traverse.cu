@@ -10,6 +10,7 @@
 // (list type, source id) order so results are deterministic run to run.
 #include <algorithm>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "engine.hpp"
@@ -383,26 +384,29 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
     k_mutual_mark<<<nb, 128, 0, s>>>(it.n_items, ncl, it.keys, it.cnt, it.off, it.code, it.seg, it.mflag, it.epair,
                                      it.unit_b, int(unit_begins.size()), T, it.pairs.p + 4);
     CSFS_LAUNCH_CHECK();
-    // pair index and partial offset: 2-counter scan over entries
-    sc.tiles.grow(scan_tile_ints(it.n_entries, 2));
+    // pair index and partial offset: 2-counter scan over entries, in 64 bits (the partial
+    // buffer passes 2^31 doubles above ~45M points)
+    sc.tiles64.grow(scan_tile_ints(it.n_entries, 2));
+    sc.grand64.grow(2);
     {
         const int* mflag = it.mflag;
         const int2* ep = it.epair;
-        auto f = [=] __device__(long long e, int* c) {
+        auto f = [=] __device__(long long e, long long* c) {
             if (mflag[e]) {
                 const int2 q = ep[e];
                 c[0] = 1;
                 c[1] = q.x >= ncl ? 2 * T.npp : (T.end[q.x] - T.begin[q.x]) + (T.end[q.y] - T.begin[q.y]);
             }
         };
-        auto count_only = [=] __device__(long long, const int*, const int*) {};
-        run_scan<2>(it.n_entries, f, count_only, sc.tiles, sc.grand, s);
-        CSFS_CK(cudaMemcpyAsync(sc.host, sc.grand.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        auto count_only = [=] __device__(long long, const long long*, const long long*) {};
+        run_scan<2, long long>(it.n_entries, f, count_only, sc.tiles64.p, sc.grand64.p, s);
+        long long tot[2] = {0, 0};
+        CSFS_CK(cudaMemcpyAsync(tot, sc.grand64.p, 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaMemcpyAsync(&it.skipped_pairs, it.pairs.p + 4, sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaStreamSynchronize(s));
-        it.n_mutual = sc.host[0];
-        it.n_partial = sc.host[1];
+        it.n_mutual = int(tot[0]);
+        it.n_partial = tot[1];
         const int np = std::max(it.n_mutual, 1);
         it.mpair.grow(np);
         it.mpoff.grow(np);
@@ -413,24 +417,25 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
         long long* poff = it.mpoff;
         int* manchor = it.manchor;
         int2* leaf = it.mleaf;
-        auto e = [=] __device__(long long i, const int* c, const int* pre) {
+        auto e = [=] __device__(long long i, const long long* c, const long long* pre) {
             if (!c[0]) return;
+            const int p = int(pre[0]);
             const int2 q = ep[i];
             if (q.x >= ncl) {  // CC: proxy sets, negative lengths
                 const int a = q.x - ncl, b = q.y - ncl;
                 const int g = needs_guard(T, T, a, true, b, true) ? kSegGuard : 0;
-                pair[pre[0]] = make_int4(a * T.npp, -(T.npp | g), b * T.npp, -T.npp);
-                manchor[pre[0]] = T.begin[a];
+                pair[p] = make_int4(a * T.npp, -(T.npp | g), b * T.npp, -T.npp);
+                manchor[p] = T.begin[a];
             } else {
                 const int g = needs_guard(T, T, q.x, false, q.y, false) ? kSegGuard : 0;
-                pair[pre[0]] = make_int4(T.begin[q.x], (T.end[q.x] - T.begin[q.x]) | g, T.begin[q.y],
-                                         T.end[q.y] - T.begin[q.y]);
-                manchor[pre[0]] = T.begin[q.x];
+                pair[p] = make_int4(T.begin[q.x], (T.end[q.x] - T.begin[q.x]) | g, T.begin[q.y],
+                                    T.end[q.y] - T.begin[q.y]);
+                manchor[p] = T.begin[q.x];
             }
-            poff[pre[0]] = pre[1];
-            leaf[pre[0]] = q;
+            poff[p] = pre[1];
+            leaf[p] = q;
         };
-        if (it.n_mutual) run_scan<2>(it.n_entries, f, e, sc.tiles, sc.grand, s);
+        if (it.n_mutual) run_scan<2, long long>(it.n_entries, f, e, sc.tiles64.p, sc.grand64.p, s);
     }
     if (it.n_mutual == 0) return;
     const int pb = ceil_div(it.n_mutual, 256);

@@ -101,7 +101,8 @@ class SumStats(C.Structure):  # summation.hpp:44-53 + B200 extras
                 ("evals_pp", C.c_uint64), ("evals_pc", C.c_uint64), ("evals_cp", C.c_uint64),
                 ("evals_cc", C.c_uint64), ("shared_tree", C.c_int),
                 ("evals_executed", C.c_uint64), ("symmetric_pairs", C.c_int),
-                ("n_ranks", C.c_int), ("t_exchange", C.c_double), ("traversal_fallback", C.c_int)]
+                ("n_ranks", C.c_int), ("t_exchange", C.c_double), ("traversal_fallback", C.c_int),
+                ("symmetric_partials", C.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -105,3 +105,30 @@ def test_c4_rk4_stage_structure(engine):
         if h is not None:
             pos = normalized(x0 + h * kq)
             zeta = z0 - 2.0 * omega * h * kq[:, 2]
+
+
+def test_partial_buffer_beyond_int32(engine):
+    """80M random points (SAL, p = 10, theta = 0.6, leaf <= 256): the symmetric-pair partial
+    buffer holds > 2^31 doubles, so its offsets must be 64-bit (traverse.cu build_mutual,
+    ADVICE r01).  The result is checked against the all-pairs sum on sampled targets (the
+    FMM error of this MAC / degree, ~1e-9) and for run-to-run bitwise reproducibility."""
+    rng = np.random.default_rng(60)
+    n = 80_000_000
+    x = rng.standard_normal((n, 3))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    w = rng.standard_normal(n) * (4 * np.pi / n)
+    cfg = TraversalConfig(mac=0.6, degree=10, n0=256)
+    k = Kernel.parse("sal")
+    p = ParticleSet(x, w)
+    st = SumStats()
+    g = engine.csfmm_sum(p, p, k, cfg, st).values
+    assert st.symmetric_pairs > 0 and st.symmetric_partials > 2**31
+    idx = np.sort(rng.choice(n, 2048, replace=False))
+    d = engine.direct_sum(ParticleSet(x[idx], np.zeros(idx.size)), p, k).values
+    e = rel_l2(g[idx], d)
+    print(f"80M random: E(FMM, direct) {e:.3e}, symmetric pairs {st.symmetric_pairs}, "
+          f"partial doubles {st.symmetric_partials}, "
+          f"{st.t_total * 1e3:.0f} ms, lists {st.pp}/{st.pc}/{st.cp}/{st.cc}")
+    assert e < 1e-8
+    g2 = engine.csfmm_sum(p, p, k, cfg).values
+    np.testing.assert_array_equal(g[idx], g2[idx])
