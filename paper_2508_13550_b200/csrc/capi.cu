@@ -6,6 +6,7 @@
 // There is no CPU fallback: without a usable sm_100a device every call fails.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -125,7 +126,16 @@ std::unique_ptr<csfs_b200_ctx> new_context(int device) {
                           std::to_string(prop.major) + std::to_string(prop.minor));
     CSFS_CK(cudaSetDevice(device));
     CSFS_CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
-    CSFS_CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    {
+        // the upward pass runs on `aux` under the traversal: the lowest priority, so the
+        // latency-bound list kernels on the critical path get the SMs first
+        int lo = 0, hi = 0;
+        CSFS_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+#ifndef CSFS_AUX_PRIORITY_LOW
+#define CSFS_AUX_PRIORITY_LOW 1
+#endif
+        CSFS_CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, CSFS_AUX_PRIORITY_LOW ? lo : 0));
+    }
     CSFS_CK(cudaEventCreateWithFlags(&c->w_copied, cudaEventDisableTiming));
     for (auto& e : c->ev) CSFS_CK(cudaEventCreate(&e));
     CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
@@ -246,14 +256,24 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
 
     // the upward pass (weights -> proxy weights) and the dual traversal (geometry -> lists)
     // are independent: the upward pass runs on the aux stream meanwhile
+    static const bool serial_up = std::getenv("CSFS_B200_TRACE_SERIAL_UPWARD") != nullptr;
     CSFS_CK(cudaStreamWaitEvent(c->aux, ev[1], 0));
-    upward_pass(S, c->cheb, c->aux);
-    CSFS_CK(cudaEventRecord(ev[2], c->aux));
+    upward_pass(S, c->cheb, serial_up ? s : c->aux);
+    CSFS_CK(cudaEventRecord(ev[2], serial_up ? s : c->aux));
+    if (serial_up) CSFS_CK(cudaEventRecord(ev[1], s));
 
+    static const bool trace = std::getenv("CSFS_B200_TRACE_LISTS") != nullptr;
     dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
+    if (trace) CSFS_CK(cudaEventRecord(ev[8], s));
     build_items(T, S, c->lists, c->items, c->sc, s);
+    if (trace) CSFS_CK(cudaEventRecord(ev[9], s));
     prepare_mutual(c, s, true);
     CSFS_CK(cudaEventRecord(ev[3], s));
+    if (trace) {
+        CSFS_CK(cudaEventSynchronize(ev[3]));
+        fprintf(stderr, "lists: traversal %.3f items %.3f mutual %.3f ms\n", ev_ms(ev[1], ev[8]), ev_ms(ev[8], ev[9]),
+                ev_ms(ev[9], ev[3]));
+    }
     CSFS_CK(cudaStreamWaitEvent(s, ev[2], 0));
 
     const int dim = c->dim;
