@@ -168,3 +168,26 @@ def test_leaf_histogram_matches_reference_tree(engine):
         want = np.bincount(sizes).tolist()
         assert engine.leaf_histogram(0) == want
         assert engine.leaf_histogram(1) == want
+
+
+@pytest.mark.parametrize("kname", ["laplace", "biot_savart"])
+def test_groups_targets_differ_from_sources(engine, kname):
+    """Separate target and source trees (no symmetric pairs): every rank count gives the
+    single-GPU engine's result bit for bit."""
+    from paper_2508_13550_b200.grids import cubed_sphere
+
+    tx, _ = cubed_sphere(6)
+    rng = np.random.default_rng(5)
+    sx = rng.standard_normal((30000, 3))
+    sx /= np.linalg.norm(sx, axis=1, keepdims=True)
+    sw = rng.standard_normal(30000)
+    k = Kernel.parse(kname)
+    cfg = TraversalConfig(mac=0.6, degree=7, n0=60)
+    t, s = ParticleSet(tx, np.zeros(len(tx))), ParticleSet(sx, sw)
+    want = engine.csfmm_sum(t, s, k, cfg).values.copy()
+    for R in (1, 2, 5):
+        g = Engine.emulated(0, R)
+        st = SumStats()
+        np.testing.assert_array_equal(g.csfmm_sum(t, s, k, cfg, st).values, want, err_msg=f"R={R}")
+        assert st.shared_tree == 0 and st.n_ranks == R
+        g.close()
