@@ -50,12 +50,16 @@ struct DevBuf {
     operator T*() const { return p; }
 };
 
-// Source segments / symmetric-pair lengths carry two flags next to the length: the sign
-// (negative = proxy points) and bit 30 of the magnitude (the coincidence guard is needed
-// for this entry; kernels_dev.cuh eval<G>).
+// Source segments / symmetric-pair lengths carry flags next to the length: the sign
+// (negative = proxy points), bit 30 of the magnitude (the coincidence guard is needed
+// for this entry; kernels_dev.cuh eval<G>) and bit 29 (the fused 1 - x.y is safe, eval<.., F>).
 constexpr int kSegGuard = 1 << 30;
-__host__ __device__ __forceinline__ int seg_len(int y) { return (y < 0 ? -y : y) & (kSegGuard - 1); }
+// bit 29: the entry's point sets are more than kFuseGap apart — the fused 1 - x.y may be used
+constexpr int kSegFused = 1 << 29;
+constexpr double kFuseGap = 4.48e-3;  // chordal; 1 - x.y >= kFuseGap^2 / 2 >= 1.0e-5
+__host__ __device__ __forceinline__ int seg_len(int y) { return (y < 0 ? -y : y) & (kSegFused - 1); }
 __host__ __device__ __forceinline__ bool seg_guard(int y) { return ((y < 0 ? -y : y) & kSegGuard) != 0; }
+__host__ __device__ __forceinline__ bool seg_fused(int y) { return ((y < 0 ? -y : y) & kSegFused) != 0; }
 
 // Raw-pointer view of a tree, passed by value into kernels.
 struct TreeView {

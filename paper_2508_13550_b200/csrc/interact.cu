@@ -38,6 +38,10 @@ namespace {
 #ifndef CSFS_IB
 #define CSFS_IB 256
 #endif
+// fused 1 - x.y on list entries whose point sets are > kFuseGap apart (engine.hpp)
+#ifndef CSFS_FUSED_DOT
+#define CSFS_FUSED_DOT 1
+#endif
 #ifndef CSFS_TPT
 #define CSFS_TPT 2
 #endif
@@ -150,7 +154,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
             // guarded: the chunk holds a segment that may contain coincident pairs
             // group g takes a contiguous share of the chunk: unit stride, so the unrolled
             // loop addresses shared memory with immediate offsets (no per-source pointer math)
-            auto compute = [&](int n, bool guarded) {
+            auto compute = [&](int n, bool guarded, bool fused) {
                 if (!any) return;
                 const int share = (n + G - 1) / G;
                 const int jb = g * share, je = min(n, jb + share);
@@ -161,6 +165,14 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
 #pragma unroll
                         for (int k = 0; k < kTPT; ++k)
                             op.template eval<true>(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, acc[k], tab);
+                    }
+                } else if (fused) {
+#pragma unroll kU
+                    for (int j = jb; j < je; ++j) {
+                        const double2 a = sxy[j], b = szw[j];
+#pragma unroll
+                        for (int k = 0; k < kTPT; ++k)
+                            op.template eval<false, true>(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, acc[k], tab);
                     }
                 } else {
 #pragma unroll kU
@@ -179,14 +191,17 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
             int ce = d.z, cpos = 0;  // cursor into the segment list (CTA-uniform)
             double rx = 0.0, ry = 0.0, rz = 0.0, rw = 0.0;
             bool fguard = false;  // guard flag of the chunk being fetched (CTA-uniform)
+            bool ffused = true;   // every segment of the chunk may use the fused 1 - x.y
             auto fetch = [&]() {
                 int filled = 0;
                 fguard = false;
+                ffused = true;
                 while (filled < kICH && ce < d.w) {
                     const int2 sg = P.seg[ce];
                     const bool sproxy = sg.y < 0;
                     const int len = seg_len(sg.y);  // 0: evaluated by the symmetric kernel
                     fguard = fguard || (len > 0 && seg_guard(sg.y));
+                    ffused = ffused && (len == 0 || seg_fused(sg.y));
                     const int take = min(len - cpos, kICH - filled);
                     if (tid >= filled && tid < filled + take) {
                         const long long src = (long long)sg.x + cpos + (tid - filled);
@@ -205,7 +220,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
                 return filled;
             };
             int n = fetch();
-            bool guarded = fguard;
+            bool guarded = fguard, fused = ffused;
             while (n > 0) {
                 if (tid < n) {
                     sxy[tid] = make_double2(rx, ry);
@@ -216,10 +231,11 @@ __global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, O
 #ifdef CSFS_FORCE_GUARD
                 guarded = CSFS_FORCE_GUARD;
 #endif
-                compute(n, guarded);
+                compute(n, guarded, CSFS_FUSED_DOT && Op::kFusable && fused);
                 __syncthreads();
                 n = next;
                 guarded = fguard;
+                fused = ffused;
             }
             if (G > 1) {
 #pragma unroll
@@ -328,6 +344,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
 #else
         const bool guarded = seg_guard(q.y);
 #endif
+        const bool fused = CSFS_FUSED_DOT && Op::kFusable && !guarded && seg_fused(q.w);
         const double* X = prox ? P.qx : P.px;
         const double* Y = prox ? P.qy : P.py;
         const double* Z = prox ? P.qz : P.pz;
@@ -371,7 +388,7 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
             // consecutive entries: one shared-memory wavefront.
             constexpr int kB = 8;
             const int qx = (lane >> 2) & 7;
-            auto sources = [&](int j, double (&c)[kB], auto kG) {
+            auto sources = [&](int j, double (&c)[kB], auto kG, auto kF) {
 #pragma unroll
                 for (int m = 0; m < kB; ++m) {
                     c[m] = 0.0;
@@ -380,7 +397,8 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
 #pragma unroll
                     for (int k = 0; k < kMTPT; ++k) {
                         double K[1];
-                        op.template value<decltype(kG)::value>(tx[k], ty[k], tz[k], a.x, a.y, b.x, K, tab);
+                        op.template value<decltype(kG)::value, decltype(kF)::value>(tx[k], ty[k], tz[k], a.x, a.y,
+                                                                                     b.x, K, tab);
                         acc[k] = fma(b.y, K[0], acc[k]);
                         c[m] = fma(tw[k], K[0], c[m]);
                     }
@@ -388,8 +406,9 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
             };
             for (int j = g * kB; j < nb; j += kB * G) {
                 double c[kB];
-                if (guarded) sources(j, c, std::true_type{});
-                else sources(j, c, std::false_type{});
+                if (guarded) sources(j, c, std::true_type{}, std::false_type{});
+                else if (fused) sources(j, c, std::false_type{}, std::true_type{});
+                else sources(j, c, std::false_type{}, std::false_type{});
                 double v4[4], v2[2];
 #pragma unroll
                 for (int m = 0; m < 4; ++m) v4[m] = c[m] + shfl_xor_d(c[m + 4], 16);
@@ -606,7 +625,7 @@ void direct_allpairs(const KernelSpec& k, const double* txyz, long long nt, cons
         CSFS_LAUNCH_CHECK();
     }
     std::vector<int2> hseg;
-    const long long kSeg = 1 << 29;  // below the guard flag bit
+    const long long kSeg = 1 << 28;  // below the fused / guard flag bits
     for (long long b = 0; b < ns; b += kSeg)
         hseg.push_back(make_int2(int(b), int(std::min(kSeg, ns - b)) | kSegGuard));
     const int nseg = int(hseg.size());

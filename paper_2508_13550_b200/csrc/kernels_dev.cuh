@@ -22,6 +22,21 @@
 
 namespace csfs_b200 {
 
+// one - x.y: F = false in the reference's unfused order (dot_ref, then one subtraction:
+// 6 FP64 instructions, the reference's rounding); F = true as three fused multiply-adds
+// (3 instructions).  Both forms are within a few ulp of 1 of the exact value, so they
+// differ by at most ~8e-16 absolutely, i.e. 8e-16 / (1 - x.y) relatively: the fused form
+// is only used on list entries whose point sets are provably more than kFuseGap apart
+// (traverse.cu can_fuse: 1 - x.y >= kFuseGap^2 / 2 = 1e-5), where the per-pair difference
+// in 1 - x.y is below 8e-11 relatively in the worst case.  Exact products
+// commute, so the fused form keeps K(t, s) = kSym K(s, t) bit for bit (the symmetric kernel).
+template <bool F>
+__device__ __forceinline__ double one_minus_dot(double one, double tx, double ty, double tz, double sx, double sy,
+                                                double sz) {
+    if (F) return fma(-tz, sz, fma(-ty, sy, fma(-tx, sx, one)));
+    return __dsub_rn(one, dot_ref(tx, ty, tz, sx, sy, sz));
+}
+
 // Each op also provides value(): the unscaled, guarded K(t, s) (0 where the guard skips),
 // used by the symmetric PP/CC path, which applies one evaluation to both the target's row
 // and the source's column; kSym: K(s, t) = kSym * K(t, s) (exactly: the unfused dot and
@@ -29,23 +44,24 @@ namespace csfs_b200 {
 // coincidence guard, for list entries proven free of pairs with 1 - x.y < 1e-14
 // (needs_guard, traverse.cu) — the same values with 5 fewer issue slots per pair.
 struct OpLaplace {
+    static constexpr bool kFusable = true;  // has a fused 1 - x.y form (one_minus_dot<true>)
     static constexpr int dim = 1;
     static constexpr int kUnroll = 16;  // k_interact source-loop unroll
     static constexpr double kSym = 1.0;
     __device__ __forceinline__ static double tgt(double x) { return x; }
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
-    template <bool G = true>
+    template <bool G = true, bool F = false>
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
-        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const double omc = one_minus_dot<F>(1.0, tx, ty, tz, sx, sy, sz);
         const bool ok = !G || not_coincident(omc);
         const double v = fast_log(G ? safe_omc(ok, omc) : omc, tab);
         K[0] = ok ? v : 0.0;
     }
-    template <bool G = true>
+    template <bool G = true, bool F = false>
     __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
                                          double* acc, const LogTable& tab) const {
-        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const double omc = one_minus_dot<F>(1.0, tx, ty, tz, sx, sy, sz);
         const bool ok = !G || not_coincident(omc);
         const double v = fast_log(G ? safe_omc(ok, omc) : omc, tab);
         acc[0] = fma(ok ? sw : 0.0, v, acc[0]);
@@ -95,19 +111,20 @@ __device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
 }
 
 struct OpBiharmonic {
+    static constexpr bool kFusable = false;  // has a fused 1 - x.y form (one_minus_dot<true>)
     static constexpr int dim = 1;
     static constexpr int kUnroll = 4;
     static constexpr double kSym = 1.0;
     __device__ __forceinline__ static double tgt(double x) { return x; }
     __device__ __forceinline__ double scale() const { return kInv4Pi; }
-    template <bool G = true>  // regular at coincidence: no guard either way
+    template <bool G = true, bool F = false>  // regular at coincidence: no guard either way
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
         const double d = dot_ref(tx, ty, tz, sx, sy, sz);
         const double u0 = __dmul_rn(0.5, __dadd_rn(1.0, d));
         K[0] = dilog_dev((u0 < 1.0) ? u0 : 1.0, tab);
     }
-    template <bool G = true>
+    template <bool G = true, bool F = false>  // the dot stays unfused (u = (1 + x.y)/2 is not cancellation-prone)
     __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
                                          double* acc, const LogTable& tab) const {
         const double d = dot_ref(tx, ty, tz, sx, sy, sz);
@@ -123,24 +140,25 @@ struct OpBiharmonic {
 };
 
 struct OpBiotSavart {
+    static constexpr bool kFusable = true;  // has a fused 1 - x.y form (one_minus_dot<true>)
     static constexpr int dim = 3;
     static constexpr double kSym = -1.0;  // cross(s, t) = -cross(t, s), 1 - s.t = 1 - t.s
     __device__ __forceinline__ static double tgt(double x) { return x; }
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
-    template <bool G = true>
+    template <bool G = true, bool F = false>
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable&) const {
-        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const double omc = one_minus_dot<F>(1.0, tx, ty, tz, sx, sy, sz);
         const bool ok = !G || not_coincident(omc);
         const double a = ok ? fast_rcp(G ? safe_omc(ok, omc) : omc) : 0.0;
         K[0] = a * __dsub_rn(__dmul_rn(ty, sz), __dmul_rn(tz, sy));
         K[1] = a * __dsub_rn(__dmul_rn(tz, sx), __dmul_rn(tx, sz));
         K[2] = a * __dsub_rn(__dmul_rn(tx, sy), __dmul_rn(ty, sx));
     }
-    template <bool G = true>
+    template <bool G = true, bool F = false>
     __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
                                          double* acc, const LogTable&) const {
-        const double omc = __dsub_rn(1.0, dot_ref(tx, ty, tz, sx, sy, sz));
+        const double omc = one_minus_dot<F>(1.0, tx, ty, tz, sx, sy, sz);
         const bool ok = !G || not_coincident(omc);
         const double a = (ok ? sw : 0.0) * fast_rcp(G ? safe_omc(ok, omc) : omc);
         // cross(x, y) unfused, in the reference's order (geometry.hpp:20-22): for close
@@ -165,6 +183,7 @@ struct OpBiotSavart {
 // kernel) is the kLogOnly instantiation: K' = log(...), scale = -pref c2.
 template <bool kLogOnly>
 struct OpSalT {
+    static constexpr bool kFusable = true;
     static constexpr int dim = 1;
     static constexpr int kUnroll = 16;
     static constexpr double kSym = 1.0;
@@ -194,18 +213,18 @@ struct OpSalT {
         const double L = fast_log(fma(s, s, s), tab);
         return kLogOnly ? L : fma(k, L, r2);
     }
-    template <bool G = true>
+    template <bool G = true, bool F = false>
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
-        const double hom = __dsub_rn(0.5, dot_ref(tx, ty, tz, sx, sy, sz));
+        const double hom = one_minus_dot<F>(0.5, tx, ty, tz, sx, sy, sz);
         const bool ok = !G || not_coincident_half(hom);
         const double v = kernel(G ? safe_omc(ok, hom) : hom, tab);
         K[0] = ok ? v : 0.0;
     }
-    template <bool G = true>
+    template <bool G = true, bool F = false>
     __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
                                          double* acc, const LogTable& tab) const {
-        const double hom = __dsub_rn(0.5, dot_ref(tx, ty, tz, sx, sy, sz));
+        const double hom = one_minus_dot<F>(0.5, tx, ty, tz, sx, sy, sz);
         const bool ok = !G || not_coincident_half(hom);
         const double v = kernel(G ? safe_omc(ok, hom) : hom, tab);
         acc[0] = fma(ok ? sw : 0.0, v, acc[0]);

@@ -75,6 +75,20 @@ __device__ __forceinline__ bool needs_guard(const TreeView& T, const TreeView& S
     return true;
 }
 
+// Can the entry use the fused 1 - x.y (kernels_dev.cuh one_minus_dot<true>)?  Only when
+// every pair of its point sets is more than kFuseGap apart (chordal, bounding spheres with
+// the particle / proxy radii): then 1 - x.y >= kFuseGap^2/2 = 1e-5 and the fused form
+// differs from the reference's unfused one by < 8e-11 relatively per pair (worst case).
+// Unit vectors only (the distance bound uses |x| = 1).
+__device__ __forceinline__ bool can_fuse(const TreeView& T, const TreeView& S, int t, bool t_prox, int s,
+                                         bool s_prox) {
+    if (*T.off_sphere || *S.off_sphere) return false;
+    const double dx = T.cx[t] - S.cx[s], dy = T.cy[t] - S.cy[s], dz = T.cz[t] - S.cz[s];
+    const double R = sqrt(dx * dx + dy * dy + dz * dz);
+    const double rt = t_prox ? T.qrad[t] : T.rad[t], rs = s_prox ? S.qrad[s] : S.rad[s];
+    return R - rt - rs > kFuseGap;
+}
+
 __global__ void k_count(const int2* __restrict__ l, long long n, int key_off, int* cnt,
                         const TreeView T, const TreeView S, int type, unsigned long long* pairs) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -162,7 +176,9 @@ __global__ void k_items(int n_items, int ncl_t, const int* __restrict__ keys,
         const int type = int(c[a] >> 32);
         const int s = int(c[a] & 0xffffffffll);
         const bool s_prox = !(type == 0 || type == 2);
-        const int g = needs_guard(T, S, t, t_prox, s, s_prox) ? kSegGuard : 0;
+        const int g = needs_guard(T, S, t, t_prox, s, s_prox) ? kSegGuard
+                      : can_fuse(T, S, t, t_prox, s, s_prox)   ? kSegFused
+                                                                : 0;
         if (!s_prox) {
             seg[b + a] = make_int2(S.begin[s], (S.end[s] - S.begin[s]) | g);
             src_pts += S.end[s] - S.begin[s];
@@ -424,12 +440,14 @@ void build_mutual(const DeviceTree& tgt, Items& it, const std::vector<long long>
             if (q.x >= ncl) {  // CC: proxy sets, negative lengths
                 const int a = q.x - ncl, b = q.y - ncl;
                 const int g = needs_guard(T, T, a, true, b, true) ? kSegGuard : 0;
-                pair[p] = make_int4(a * T.npp, -(T.npp | g), b * T.npp, -T.npp);
+                const int fz = !g && can_fuse(T, T, a, true, b, true) ? kSegFused : 0;
+                pair[p] = make_int4(a * T.npp, -(T.npp | g), b * T.npp, -(T.npp | fz));
                 manchor[p] = T.begin[a];
             } else {
                 const int g = needs_guard(T, T, q.x, false, q.y, false) ? kSegGuard : 0;
+                const int fz = !g && can_fuse(T, T, q.x, false, q.y, false) ? kSegFused : 0;
                 pair[p] = make_int4(T.begin[q.x], (T.end[q.x] - T.begin[q.x]) | g, T.begin[q.y],
-                                    T.end[q.y] - T.begin[q.y]);
+                                    (T.end[q.y] - T.begin[q.y]) | fz);
                 manchor[p] = T.begin[q.x];
             }
             poff[p] = pre[1];
