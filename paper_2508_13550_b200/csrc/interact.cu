@@ -65,6 +65,19 @@ template <class Op>
 struct UnrollOf<Op, std::void_t<decltype(Op::kUnroll)>> {
     static constexpr int value = Op::kUnroll;
 };
+// resident CTAs per SM k_interact is compiled for, per functor (Op::kMinBlocks, else
+// CSFS_MINB): three (80 registers, 3 x 73 KB of shared memory) for Laplace and the
+// biharmonic kernel — C2 -4.7%, C3 -4.3% — two (124 registers) for SAL, whose deeper
+// unrolled loop loses 1% at 80 registers, and for Biot-Savart (its 3-component reduction
+// buffer leaves no room for a third CTA)
+template <class Op, class = void>
+struct MinBlocksOf {
+    static constexpr int value = CSFS_MINB;
+};
+template <class Op>
+struct MinBlocksOf<Op, std::void_t<decltype(Op::kMinBlocks)>> {
+    static constexpr int value = Op::kMinBlocks;
+};
 #ifndef CSFS_MTPT
 #define CSFS_MTPT 2
 #endif
@@ -93,11 +106,17 @@ struct InteractParams {
 };
 
 template <class Op>
-__global__ void __launch_bounds__(kIB, CSFS_MINB) k_interact(InteractParams P, Op op) {
+__global__ void __launch_bounds__(kIB, MinBlocksOf<Op>::value) k_interact(InteractParams P, Op op) {
     constexpr int D = Op::dim;
     constexpr int kU = UnrollOf<Op>::value;
-    __shared__ double2 sxy[kICH], szw[kICH];
-    __shared__ double red[kIB * kTPT * D];
+    // the group reduction after the source loop reuses the source buffers for scalar kernels
+    // (D == 1: 4 KB of 8), so three CTAs (3 x (64 KB table + 8 KB)) fit one SM's 228 KB
+    __shared__ double2 sbuf[2 * kICH];
+    __shared__ double red_own[D == 1 ? 1 : kIB * kTPT * D];
+    double2* const sxy = sbuf;
+    double2* const szw = sbuf + kICH;
+    double* const red = D == 1 ? reinterpret_cast<double*>(sbuf) : red_own;
+    static_assert(D != 1 || kIB * kTPT * sizeof(double) <= sizeof(double2) * 2 * kICH, "red fits the source buffers");
     extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
     __shared__ int item_sh;
     const int tid = threadIdx.x;

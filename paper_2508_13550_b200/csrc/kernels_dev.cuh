@@ -44,6 +44,7 @@ __device__ __forceinline__ double one_minus_dot(double one, double tx, double ty
 // coincidence guard, for list entries proven free of pairs with 1 - x.y < 1e-14
 // (needs_guard, traverse.cu) — the same values with 5 fewer issue slots per pair.
 struct OpLaplace {
+    static constexpr int kMinBlocks = 3;  // k_interact CTAs per SM (interact.cu MinBlocksOf)
     static constexpr bool kFusable = true;  // has a fused 1 - x.y form (one_minus_dot<true>)
     static constexpr int dim = 1;
     static constexpr int kUnroll = 16;  // k_interact source-loop unroll
@@ -111,6 +112,7 @@ __device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
 }
 
 struct OpBiharmonic {
+    static constexpr int kMinBlocks = 3;
     static constexpr bool kFusable = false;  // has a fused 1 - x.y form (one_minus_dot<true>)
     static constexpr int dim = 1;
     static constexpr int kUnroll = 4;
