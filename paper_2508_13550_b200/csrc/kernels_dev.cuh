@@ -184,10 +184,17 @@ struct OpBiotSavart {
 // (the factor 2 comes from the halved targets, below).  The c1 == 0 case (pure log
 // kernel) is the kLogOnly instantiation: K' = log(...), scale = -pref c2.
 template <bool kLogOnly>
+#ifndef CSFS_SAL_UNROLL
+#define CSFS_SAL_UNROLL 16
+#endif
+#ifndef CSFS_SAL_MINB
+#define CSFS_SAL_MINB 2
+#endif
 struct OpSalT {
     static constexpr bool kFusable = true;
     static constexpr int dim = 1;
-    static constexpr int kUnroll = 16;
+    static constexpr int kUnroll = CSFS_SAL_UNROLL;
+    static constexpr int kMinBlocks = CSFS_SAL_MINB;
     static constexpr double kSym = 1.0;
     double scale_, k;
     __host__ static OpSalT make(double pref, double c1, double c2) {
