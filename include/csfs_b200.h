@@ -239,7 +239,9 @@ CSFS_B200_API int csfs_b200_evaluate_tree(csfs_b200_ctx* ctx, const csfs_b200_tr
  *   _create_emulated  nranks ranks on ONE device, run phase by phase with device copies in
  *                     place of NCCL: the partition and exchange layout, bitwise, on one
  *                     GPU (tests / per-rank cost measurement; not a speed-up).
- * A failing NCCL call returns CSFS_B200_NCCL_ERROR (3). */
+ * A failing NCCL call returns CSFS_B200_NCCL_ERROR (3).  In a multi-device group a rank
+ * that fails aborts every communicator so no rank is left waiting in an all-gather; the
+ * group then returns errors until it is destroyed. */
 #define CSFS_B200_NCCL_ID_BYTES 128
 CSFS_B200_API int csfs_b200_create_multi(csfs_b200_ctx** out, int num_gpus, const int* device_ids);
 CSFS_B200_API int csfs_b200_nccl_unique_id(unsigned char* id);

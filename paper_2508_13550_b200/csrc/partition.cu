@@ -27,6 +27,7 @@
 //             phase in lockstep (parity tests of the partition / exchange layout on one
 //             GPU; never ranks that wait on each other on one device)
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <exception>
 #include <thread>
@@ -387,18 +388,30 @@ void run_csfmm_group(Ctx* c, const double* txyz, size_t nt, const double* sxyz, 
     } else {  // Multi: one host thread per device; rank 0 here on the caller's stream
         std::vector<std::exception_ptr> errs(ranks.size());
         std::vector<std::thread> th;
+        std::atomic<bool> aborted{false};
+        // a rank that fails would leave the others waiting inside an all-gather forever:
+        // the first failure aborts every communicator, which unblocks them with an NCCL
+        // error (the group is unusable afterwards; csfs_b200.h)
+        auto fail_all = [&] {
+            if (aborted.exchange(true)) return;
+            for (Ctx* r : ranks)
+                if (r->comm) ncclCommAbort(r->comm);
+            for (Ctx* r : ranks) r->comm = nullptr;
+        };
         for (size_t r = 1; r < ranks.size(); ++r)
             th.emplace_back([&, r] {
                 try {
                     rank_program(ranks[r], in0, same_xyz, ks, f, nullptr, ranks[r]->own, count_exec);
                 } catch (...) {
                     errs[r] = std::current_exception();
+                    fail_all();
                 }
             });
         try {
             rank_program(c, in0, same_xyz, ks, f, out, s, count_exec);
         } catch (...) {
             errs[0] = std::current_exception();
+            fail_all();
         }
         for (auto& t : th) t.join();
         CSFS_CK(cudaSetDevice(c->device));
