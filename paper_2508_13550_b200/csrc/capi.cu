@@ -138,7 +138,7 @@ std::unique_ptr<csfs_b200_ctx> new_context(int device) {
     }
     CSFS_CK(cudaEventCreateWithFlags(&c->w_copied, cudaEventDisableTiming));
     for (auto& e : c->ev) CSFS_CK(cudaEventCreate(&e));
-    CSFS_CK(cudaMallocHost(&c->sc.host, 64 * sizeof(int)));
+    CSFS_CK(cudaMallocHost(&c->sc.host, kHostInts * sizeof(int)));
     const char* nosym = std::getenv("CSFS_B200_NO_SYMMETRIC");
     c->use_mutual = !(nosym && nosym[0] == '1');
     const char* scope = std::getenv("CSFS_B200_MUTUAL_SCOPE");

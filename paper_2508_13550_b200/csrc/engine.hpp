@@ -118,7 +118,20 @@ struct Scratch {
     int* host = nullptr;    // pinned host mirror for small read-backs
     DevBuf<double> fxi, feta;  // level-0 face coordinates in input order
     DevBuf<int> fface;
+    // label-then-sort build (tree.cu): per-particle labels / leaves / sort keys and radix
+    // scratch (input order); per (cluster, quadrant) child ids, counts and bounds; level
+    // descriptors {first, cnt, nsplit, overflow}
+    DevBuf<int> lab, leaf, key, kb, vb, sorted, hist, qchild, scnt, cbase;
+    DevBuf<unsigned long long> sbnd;
+    DevBuf<int4> lev;
+    DevBuf<int> rcnt;
+    int qcap = 0;  // clusters the per-quadrant arrays hold
 };
+// sc.host layout (pinned ints): [0, 64) small read-backs, [kHostLev, +4 * kMaxDepth + 16)
+// level descriptors, [kHostRoots, +6) root counts
+constexpr int kHostLev = 256;
+constexpr int kHostRoots = 768;
+constexpr int kHostInts = 1024;
 
 // Interaction lists in internal cluster ids, (t, s) pairs, canonical after build.
 struct Lists {

@@ -16,8 +16,14 @@
 // Internal cluster ids are level-major (BFS); reference_ids() maps them onto the
 // reference's LIFO numbering for export (K5).  Particle data stays SoA in HBM.
 #include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
 
 #include "engine.hpp"
+#include "radix.cuh"
 #include "scan.cuh"
 
 namespace csfs_b200 {
@@ -228,12 +234,7 @@ __global__ void k_bounds(long long n, int first, const int* nnew_dev, int cnt_ho
 }
 
 // Bounds -> interpolant rectangle, centre (:65-66) and the split decision (:95-96).
-__global__ void k_geom(int first, const int* nnew_dev, int cnt_host, ClusterPtrs c, bool shrink,
-                       int n0, int* nsplit) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const int cnt = nnew_dev ? *nnew_dev : cnt_host;
-    if (j >= cnt) return;
-    const int id = first + j;
+__device__ __forceinline__ bool geom_one(const ClusterPtrs& c, int id, bool shrink, int n0) {
     const int count = c.end[id] - c.begin[id];
     double x0 = c.xi0[id], x1 = c.xi1[id], e0 = c.eta0[id], e1 = c.eta1[id];
     if (shrink && count > 0) {
@@ -257,7 +258,16 @@ __global__ void k_geom(int first, const int* nnew_dev, int cnt_host, ClusterPtrs
     const double ext = (ex < ey) ? ey : ex;  // std::max
     const bool sp = !(count <= n0 || c.depth[id] >= kMaxDepth) && !(ext < kMinExtent);
     c.split[id] = sp ? 1 : 0;
-    if (sp) atomicAdd(nsplit, 1);
+    return sp;
+}
+
+__global__ void k_geom(int first, const int* nnew_dev, int cnt_host, ClusterPtrs c, bool shrink,
+                       int n0, int* nsplit) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cnt = nnew_dev ? *nnew_dev : cnt_host;
+    if (j >= cnt) return;
+    const int id = first + j;
+    if (geom_one(c, id, shrink, n0)) atomicAdd(nsplit, 1);
 }
 
 // Radii of every cluster once the tree is final (:67-69), by leaf: one warp per leaf computes its particles' chordal distances to the leaf's
@@ -281,12 +291,19 @@ __global__ void k_radius_leaf(int ncl, const int* __restrict__ nchild, const int
             const double dx = __dsub_rn(ax, px[i]);
             const double dy = __dsub_rn(ay, py[i]);
             const double dz = __dsub_rn(az, pz[i]);
-            const unsigned long long v = __double_as_longlong(__dsqrt_rn(dot_ref(dx, dy, dz, dx, dy, dz)));
+            // the squared distance: sqrt is monotone, so sqrt(max d^2) = max sqrt(d^2) bit for bit
+            // (one correctly rounded sqrt per cluster, k_rad_sqrt, instead of one per distance)
+            const unsigned long long v = __double_as_longlong(dot_ref(dx, dy, dz, dx, dy, dz));
             m = v > m ? v : m;
         }
         m = warp_max_u64(m);
         if (lane == 0 && b < e) atomicMax(&radu[a], m);
     }
+}
+
+__global__ void k_rad_sqrt(int ncl, double* rad) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < ncl) rad[c] = __dsqrt_rn(rad[c]);
 }
 
 __global__ void k_gather_xyz(long long n, const int* __restrict__ perm, const double* __restrict__ xyz,
@@ -540,6 +557,398 @@ __global__ void k_fill_node(int ncl, const int* __restrict__ begin, const int* _
     for (int i = begin[c] + threadIdx.x; i < end[c]; i += blockDim.x) node[i] = c;
 }
 
+// --- label-then-sort build (the default) --------------------------------------------------
+// Particles never move while the levels are decided.  Each particle keeps a label in input
+// order: a cluster id (>= 0), or -(4 p + q + 1) = "quadrant q of splitting cluster p", which
+// resolves through qchild[4 p + q] once the next level is allocated.  Per level:
+//   k_label : particles of splitting frontier clusters take their quadrant label; per
+//             (cluster, quadrant) the count and the shrunk bounds accumulate with atomics
+//             (integer min/max on order-preserving encodings: exact and order independent),
+//             aggregated over the lanes of a warp that share a quadrant (match_any + redux);
+//   k_alloc : one CTA allocates the children of the whole frontier in parent and quadrant
+//             order (empties pruned: cluster_tree.cpp:124-140), sets their ranges from the
+//             quadrant counts, bounds, centres and split decisions, and writes the next
+//             level's descriptor — so no level needs the host.
+// After the last level ONE stable sort of the particles by their leaf's begin yields the
+// reference's order: the composition of its stable 4-way partitions keeps every leaf's
+// particles in input order.
+struct LevelDesc {
+    int first, cnt, nsplit, ovf;
+};
+
+__device__ __forceinline__ unsigned long long redux_min_u64(unsigned m, unsigned long long v) {
+    const unsigned hi = unsigned(v >> 32);
+    const unsigned mh = __reduce_min_sync(m, hi);
+    const unsigned ml = __reduce_min_sync(m, hi == mh ? unsigned(v) : 0xffffffffu);
+    return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned long long redux_max_u64(unsigned m, unsigned long long v) {
+    const unsigned hi = unsigned(v >> 32);
+    const unsigned mh = __reduce_max_sync(m, hi);
+    const unsigned ml = __reduce_max_sync(m, hi == mh ? unsigned(v) : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+
+// Per-(cluster, quadrant) counts and bounds over a tile of kTile consecutive particles.
+// The particles' slots and face coordinates are first staged in shared memory with
+// coalesced loads (phase A, one particle per thread per step); then each thread walks kRun
+// CONSECUTIVE staged particles, keeping count and bounds in registers while the slot stays
+// the same (a change flushes the finished run with atomics: integer min/max on
+// order-preserving encodings, exact and order independent).  A tile whose particles all
+// share one slot (the top levels on coherent inputs) is reduced over the CTA and issues one
+// set of atomics; otherwise the lanes whose last runs share a slot combine them
+// (match_any + redux) and one of them issues the atomics.
+constexpr int kRun = 8;
+constexpr int kRunThreads = 256;
+constexpr int kTile = kRun * kRunThreads;
+constexpr int kTilePad = kTile + kTile / kRun;
+__device__ __forceinline__ int tpad(int e) { return e + e / kRun; }  // conflict-free per-thread runs
+
+struct RunAcc {
+    int key = -1, cnt = 0;
+    unsigned long long lo_x = 0, hi_x = 0, lo_e = 0, hi_e = 0;
+};
+
+__device__ __forceinline__ void run_flush(const RunAcc& r, int* cnt, unsigned long long* bnd) {
+    atomicAdd(&cnt[r.key], r.cnt);
+    atomicMin(&bnd[4ll * r.key + 0], r.lo_x);
+    atomicMax(&bnd[4ll * r.key + 1], r.hi_x);
+    atomicMin(&bnd[4ll * r.key + 2], r.lo_e);
+    atomicMax(&bnd[4ll * r.key + 3], r.hi_e);
+}
+
+struct TileStage {
+    int key[kTilePad];
+    double x[kTilePad], e[kTilePad];
+};
+
+__device__ __forceinline__ void tile_accumulate(const TileStage& st, int* cnt, unsigned long long* bnd) {
+    RunAcc r;
+    bool flushed = false;
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) {
+        const int p = tpad(threadIdx.x * kRun + j);
+        const int key = st.key[p];
+        if (key < 0) continue;
+        const unsigned long long ux = ord_enc(st.x[p]), ue = ord_enc(st.e[p]);
+        if (key != r.key) {
+            if (r.key >= 0) {
+                run_flush(r, cnt, bnd);
+                flushed = true;
+            }
+            r.key = key;
+            r.cnt = 1;
+            r.lo_x = r.hi_x = ux;
+            r.lo_e = r.hi_e = ue;
+        } else {
+            ++r.cnt;
+            r.lo_x = ux < r.lo_x ? ux : r.lo_x;
+            r.hi_x = ux > r.hi_x ? ux : r.hi_x;
+            r.lo_e = ue < r.lo_e ? ue : r.lo_e;
+            r.hi_e = ue > r.hi_e ? ue : r.hi_e;
+        }
+    }
+    const int key0 = st.key[0];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (__syncthreads_and(key0 >= 0 && !flushed && (r.key == key0 || r.key < 0))) {
+        // one slot for the whole tile: CTA reduction, one set of atomics
+        __shared__ unsigned long long red[kRunThreads / 32][5];
+        const unsigned long long v[5] = {(unsigned long long)(r.key < 0 ? 0 : r.cnt), r.key < 0 ? ~0ull : r.lo_x,
+                                         r.key < 0 ? 0ull : r.hi_x, r.key < 0 ? ~0ull : r.lo_e,
+                                         r.key < 0 ? 0ull : r.hi_e};
+        const unsigned long long c = __reduce_add_sync(0xffffffffu, unsigned(v[0]));
+        const unsigned long long a0 = redux_min_u64(0xffffffffu, v[1]), a1 = redux_max_u64(0xffffffffu, v[2]);
+        const unsigned long long a2 = redux_min_u64(0xffffffffu, v[3]), a3 = redux_max_u64(0xffffffffu, v[4]);
+        if (lane == 0) {
+            red[w][0] = c;
+            red[w][1] = a0;
+            red[w][2] = a1;
+            red[w][3] = a2;
+            red[w][4] = a3;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            RunAcc t;
+            t.key = key0;
+            unsigned long long cc = 0;
+            t.lo_x = t.lo_e = ~0ull;
+            for (int k = 0; k < kRunThreads / 32; ++k) {
+                cc += red[k][0];
+                t.lo_x = red[k][1] < t.lo_x ? red[k][1] : t.lo_x;
+                t.hi_x = red[k][2] > t.hi_x ? red[k][2] : t.hi_x;
+                t.lo_e = red[k][3] < t.lo_e ? red[k][3] : t.lo_e;
+                t.hi_e = red[k][4] > t.hi_e ? red[k][4] : t.hi_e;
+            }
+            t.cnt = int(cc);
+            run_flush(t, cnt, bnd);
+        }
+        return;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, r.key);
+    if (r.key < 0) return;
+    RunAcc t = r;
+    t.cnt = int(__reduce_add_sync(peers, unsigned(r.cnt)));
+    t.lo_x = redux_min_u64(peers, r.lo_x);
+    t.hi_x = redux_max_u64(peers, r.hi_x);
+    t.lo_e = redux_min_u64(peers, r.lo_e);
+    t.hi_e = redux_max_u64(peers, r.hi_e);
+    if ((peers & ((1u << lane) - 1u)) == 0) run_flush(t, cnt, bnd);
+}
+
+__global__ void k_root_init(ClusterPtrs c, int* rcnt) {
+    const int k = threadIdx.x;
+    if (k < 6) {
+        rcnt[k] = 0;
+        c.bnd[4 * k + 0] = ~0ull;
+        c.bnd[4 * k + 1] = 0ull;
+        c.bnd[4 * k + 2] = ~0ull;
+        c.bnd[4 * k + 3] = 0ull;
+    }
+}
+
+// Level 0 (cluster_tree.cpp:35-50): face coordinates, the face label, and the six roots'
+// counts and bounds.  Also flags points off the unit sphere (see k_face).
+__global__ void __launch_bounds__(kRunThreads)
+    k_face_label(const double* __restrict__ xyz, long long n, double* fxi, double* feta, int* lab, int* off_sphere,
+                 int* rcnt, unsigned long long* rbnd) {
+    __shared__ TileStage st;
+    const long long base = (long long)blockIdx.x * kTile;
+    bool off = false;
+#pragma unroll 2
+    for (int j = 0; j < kRun; ++j) {
+        const int el = j * kRunThreads + threadIdx.x;
+        const long long i = base + el;
+        int f = -1;
+        double a = 0.0, b = 0.0;
+        if (i < n) {
+            const double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+            face_project(x, y, z, f, a, b);
+            fxi[i] = a;
+            feta[i] = b;
+            lab[i] = f;
+            off = off || !(fabs(x * x + y * y + z * z - 1.0) <= 1e-12);
+        }
+        const int p = tpad(el);
+        st.key[p] = f;
+        st.x[p] = a;
+        st.e[p] = b;
+    }
+    if (off) atomicOr(off_sphere, 1);
+    __syncthreads();
+    tile_accumulate(st, rcnt, rbnd);
+}
+
+// The six roots (:71-82): ranges in face order, face squares, shrunk bounds, centres and
+// split decisions; level 0's descriptor; the roots' quadrant accumulators.
+__global__ void k_root_geom(ClusterPtrs c, const int* rcnt, bool shrink, int n0, LevelDesc* lev, int* scnt,
+                            unsigned long long* sbnd) {
+    __shared__ int nsp;
+    const int k = threadIdx.x;
+    if (k == 0) nsp = 0;
+    __syncthreads();
+    if (k < 6) {
+        int b = 0;
+        for (int j = 0; j < k; ++j) b += rcnt[j];
+        c.face[k] = k;
+        c.depth[k] = 0;
+        c.begin[k] = b;
+        c.end[k] = b + rcnt[k];
+        c.parent[k] = -1;
+        c.nchild[k] = 0;
+        c.child[k] = make_int4(-1, -1, -1, -1);
+        c.xi0[k] = -kPi / 4.0;
+        c.xi1[k] = kPi / 4.0;
+        c.eta0[k] = -kPi / 4.0;
+        c.eta1[k] = kPi / 4.0;
+        c.rad[k] = 0.0;
+        if (geom_one(c, k, shrink, n0)) atomicAdd(&nsp, 1);
+        for (int q = 0; q < 4; ++q) {
+            scnt[4 * k + q] = 0;
+            sbnd[16 * k + 4 * q + 0] = ~0ull;
+            sbnd[16 * k + 4 * q + 1] = 0ull;
+            sbnd[16 * k + 4 * q + 2] = ~0ull;
+            sbnd[16 * k + 4 * q + 3] = 0ull;
+        }
+    }
+    __syncthreads();
+    if (k == 0) lev[0] = LevelDesc{0, 6, nsp, 0};
+}
+
+// Level d: quadrant labels of the particles of splitting frontier clusters (:97-100).
+// Phase A is written as three independent sweeps over the thread's kRun particles (labels
+// and face coordinates, then label resolution, then the quadrant test) so that each
+// sweep's loads are all in flight together.
+__global__ void __launch_bounds__(kRunThreads)
+    k_label(long long n, int d, const LevelDesc* __restrict__ lev, ClusterPtrs c, const double* __restrict__ fxi,
+            const double* __restrict__ feta, int* lab, const int* __restrict__ qchild, int* scnt,
+            unsigned long long* sbnd) {
+    const LevelDesc L = lev[d];
+    if (L.nsplit == 0) return;
+    __shared__ TileStage st;
+    const long long base = (long long)blockIdx.x * kTile + threadIdx.x;
+    int v[kRun], nd[kRun];
+    double x[kRun], e[kRun];
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) {
+        const long long i = base + j * kRunThreads;
+        const bool in = i < n;
+        v[j] = in ? lab[i] : INT_MAX;
+        x[j] = in ? fxi[i] : 0.0;
+        e[j] = in ? feta[i] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) nd[j] = v[j] < 0 ? qchild[-v[j] - 1] : v[j];
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) {
+        const long long i = base + j * kRunThreads;
+        int key = -1;
+        if (nd[j] >= L.first && nd[j] < L.first + L.cnt && c.split[nd[j]]) {
+            key = 4 * nd[j] + quadrant_of(c, nd[j], x[j], e[j]);
+            lab[i] = -(key + 1);
+        } else if (v[j] < 0) {
+            lab[i] = nd[j];
+        }
+        const int p = tpad(j * kRunThreads + threadIdx.x);
+        st.key[p] = key;
+        st.x[p] = x[j];
+        st.e[p] = e[j];
+    }
+    __syncthreads();
+    tile_accumulate(st, scnt, sbnd);
+}
+
+// Level d's children (:124-140) in two launches: one CTA scans the frontier's non-empty
+// quadrant counts into first child ids (parent order, empties pruned); then one thread per
+// (frontier cluster, quadrant) creates its child.
+constexpr int kAllocThreads = 1024;
+constexpr int kAllocItems = 4;
+
+__global__ void __launch_bounds__(kAllocThreads)
+    k_alloc_scan(int d, LevelDesc* lev, ClusterPtrs c, const int* __restrict__ scnt, int* cbase, int cap) {
+    const LevelDesc L = lev[d];
+    const int next = L.first + L.cnt;
+    if (L.nsplit == 0) {
+        if (threadIdx.x == 0) lev[d + 1] = LevelDesc{next, 0, 0, 0};
+        return;
+    }
+    int carry = 0;
+    for (int f0 = 0; f0 < L.cnt; f0 += kAllocThreads * kAllocItems) {
+        int m[kAllocItems], tot = 0;
+#pragma unroll
+        for (int j = 0; j < kAllocItems; ++j) {
+            const int f = f0 + threadIdx.x * kAllocItems + j;
+            m[j] = 0;
+            if (f < L.cnt && c.split[L.first + f]) {
+                const int4 q = reinterpret_cast<const int4*>(scnt)[L.first + f];
+                m[j] = (q.x > 0) + (q.y > 0) + (q.z > 0) + (q.w > 0);
+            }
+            tot += m[j];
+        }
+        int v[1] = {tot}, all[1];
+        block_exclusive_scan<1, kAllocThreads>(v, all);
+        int b = next + carry + v[0];
+#pragma unroll
+        for (int j = 0; j < kAllocItems; ++j) {
+            const int f = f0 + threadIdx.x * kAllocItems + j;
+            if (f < L.cnt) cbase[f] = b;
+            b += m[j];
+        }
+        carry += all[0];
+    }
+    if (threadIdx.x == 0) {
+        const bool ovf = (long long)next + carry > cap;
+        lev[d + 1] = LevelDesc{next, ovf ? 0 : carry, 0, ovf ? 1 : 0};
+    }
+}
+
+__global__ void k_alloc_fill(int d, LevelDesc* lev, ClusterPtrs c, const int* __restrict__ scnt, int* scnt_w,
+                             unsigned long long* sbnd, const int* __restrict__ cbase, int* qchild, bool shrink,
+                             int n0) {
+    const LevelDesc L = lev[d];
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    bool sp = false;
+    if (L.nsplit > 0 && !lev[d + 1].ovf && g < 4 * L.cnt) {
+        const int f = g >> 2, q = g & 3, id = L.first + f;
+        if (c.split[id]) {
+            const int4 cq4 = reinterpret_cast<const int4*>(scnt)[id];
+            const int cq[4] = {cq4.x, cq4.y, cq4.z, cq4.w};
+            int acc = c.begin[id], k = 0;
+            for (int p = 0; p < q; ++p) {
+                acc += cq[p];
+                k += cq[p] > 0;
+            }
+            const int cid = cbase[f] + k;
+            const int slot = 4 * id + q;
+            qchild[slot] = cq[q] > 0 ? cid : -1;
+            if (q == 0) {  // the parent's child list (quadrant order, empties pruned)
+                int ch[4] = {-1, -1, -1, -1}, m = 0;
+                for (int p = 0; p < 4; ++p)
+                    if (cq[p] > 0) {
+                        ch[m] = cbase[f] + m;
+                        ++m;
+                    }
+                c.child[id] = make_int4(ch[0], ch[1], ch[2], ch[3]);
+                c.nchild[id] = m;
+            }
+            if (cq[q] > 0) {
+                const double x0 = c.xi0[id], x1 = c.xi1[id], e0 = c.eta0[id], e1 = c.eta1[id];
+                const double mx = __dmul_rn(0.5, __dadd_rn(x0, x1));
+                const double my = __dmul_rn(0.5, __dadd_rn(e0, e1));
+                c.face[cid] = c.face[id];
+                c.depth[cid] = c.depth[id] + 1;
+                c.begin[cid] = acc;
+                c.end[cid] = acc + cq[q];
+                c.parent[cid] = id;
+                c.nchild[cid] = 0;
+                c.child[cid] = make_int4(-1, -1, -1, -1);
+                c.xi0[cid] = (q & 1) ? mx : x0;
+                c.xi1[cid] = (q & 1) ? x1 : mx;
+                c.eta0[cid] = (q & 2) ? my : e0;
+                c.eta1[cid] = (q & 2) ? e1 : my;
+                c.rad[cid] = 0.0;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) c.bnd[4ll * cid + v] = sbnd[4ll * slot + v];
+                sp = geom_one(c, cid, shrink, n0);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {  // the child's own quadrant accumulators
+                    scnt_w[4 * cid + v] = 0;
+                    sbnd[16ll * cid + 4 * v + 0] = ~0ull;
+                    sbnd[16ll * cid + 4 * v + 1] = 0ull;
+                    sbnd[16ll * cid + 4 * v + 2] = ~0ull;
+                    sbnd[16ll * cid + 4 * v + 3] = 0ull;
+                }
+            }
+        }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, sp);
+    if (b && (threadIdx.x & 31) == 0) atomicAdd(&lev[d + 1].nsplit, __popc(b));
+}
+
+// Final labels -> sort keys (the leaf's first tree-order slot).
+__global__ void k_leaf_key(long long n, const int* __restrict__ lab, const int* __restrict__ qchild,
+                           const int* __restrict__ begin, int* key) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int v = lab[i];
+    key[i] = begin[v < 0 ? qchild[-v - 1] : v];
+}
+
+// Tree order: perm, face coordinates and positions through the sorted positions.  (The
+// per-particle leaf, DeviceTree::node, is only kept by the level build, which needs it.)
+__global__ void k_gather_tree(long long n, const int* __restrict__ sorted, const double* __restrict__ fxi,
+                              const double* __restrict__ feta, const double* __restrict__ xyz, int* perm,
+                              double* xi, double* eta, double* px, double* py, double* pz) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int i = sorted[t];
+    perm[t] = i;
+    xi[t] = fxi[i];
+    eta[t] = feta[i];
+    px[t] = xyz[3ll * i];
+    py[t] = xyz[3ll * i + 1];
+    pz[t] = xyz[3ll * i + 2];
+}
+
 // Proxy points (interpolation.cpp:51-68): mapped nodes mid + half*s_k, pushed to the sphere.
 __global__ void k_proxy(int ncl, int np, Cheb cheb, const int* __restrict__ face,
                         const double* __restrict__ xi0, const double* __restrict__ xi1,
@@ -683,9 +1092,14 @@ TreeView DeviceTree::view() const {
     return v;
 }
 
-void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_in, long long n,
-                int degree, int n0, bool shrink, const Cheb& cheb, cudaStream_t s,
-                cudaEvent_t w_ready) {
+static void finish_tree(DeviceTree& t, const double* w_in, long long n, const Cheb& cheb, cudaStream_t s,
+                        cudaEvent_t w_ready);
+
+// The level-synchronous build of rounds 1-2 (particles partitioned level by level, one host
+// read-back per level); CSFS_B200_TREE=levels selects it (A/B and cross-check of the default).
+static void build_tree_levels(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_in, long long n,
+                              int degree, int n0, bool shrink, const Cheb& cheb, cudaStream_t s,
+                              cudaEvent_t w_ready) {
     t.n = n;
     t.degree = degree;
     t.np = degree + 1;
@@ -875,8 +1289,17 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
     // ---- positions in tree order, then every cluster's radius ------------------------------
     k_gather_xyz<<<gp, kThreads, 0, s>>>(n, t.perm, xyz, t.px, t.py, t.pz);
     CSFS_LAUNCH_CHECK();
+    finish_tree(t, w_in, n, cheb, s, w_ready);
+}
+
+// Radii, weights in tree order and proxy points of a tree whose particles are in tree order.
+static void finish_tree(DeviceTree& t, const double* w_in, long long n, const Cheb& cheb, cudaStream_t s,
+                        cudaEvent_t w_ready) {
+    const int gp = ceil_div(n, kThreads);
     k_radius_leaf<<<ceil_div((long long)t.ncl * 32, 128), 128, 0, s>>>(t.ncl, t.nchild, t.begin, t.end, t.parent,
                                                                       t.px, t.py, t.pz, t.cx, t.cy, t.cz, t.rad);
+    CSFS_LAUNCH_CHECK();
+    k_rad_sqrt<<<ceil_div(t.ncl, kThreads), kThreads, 0, s>>>(t.ncl, t.rad);
     CSFS_LAUNCH_CHECK();
 
     // ---- weights in tree order (permute_weights, summation.cpp:98-104) ---------------------
@@ -899,6 +1322,136 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
     k_qrad<<<ceil_div((long long)t.ncl * 32, kThreads), kThreads, 0, s>>>(t.ncl, t.npp, t.cx, t.cy, t.cz, t.qx, t.qy,
                                                                           t.qz, t.qrad);
     CSFS_LAUNCH_CHECK();
+}
+
+// Grows the per-(cluster, quadrant) arrays with the cluster arrays, keeping `used` clusters.
+static void reserve_quadrants(Scratch& sc, int cap, int used, cudaStream_t s) {
+    if (cap <= sc.qcap) return;
+    sc.qchild.grow_keep(4 * size_t(cap), 4 * size_t(used), s);
+    sc.scnt.grow_keep(4 * size_t(cap), 4 * size_t(used), s);
+    sc.sbnd.grow_keep(16 * size_t(cap), 16 * size_t(used), s);
+    sc.qcap = cap;
+}
+
+void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_in, long long n, int degree,
+                int n0, bool shrink, const Cheb& cheb, cudaStream_t s, cudaEvent_t w_ready) {
+    {
+        const char* e = std::getenv("CSFS_B200_TREE");  // read per call: tests flip it
+        if (e && std::string(e) == "levels") {
+            build_tree_levels(t, sc, xyz, w_in, n, degree, n0, shrink, cheb, s, w_ready);
+            return;
+        }
+    }
+    t.n = n;
+    t.degree = degree;
+    t.np = degree + 1;
+    t.npp = t.np * t.np;
+    t.n0 = n0;
+    t.shrink = shrink;
+    t.has_w = w_in != nullptr;
+    t.ncl = 0;
+    t.level_first.clear();
+    t.level_count.clear();
+    for (DevBuf<double>* b : {&t.px, &t.py, &t.pz, &t.xi, &t.eta, &sc.fxi, &sc.feta}) b->grow(n);
+    for (DevBuf<int>* b : {&t.perm, &sc.lab, &sc.key, &sc.kb, &sc.vb, &sc.sorted}) b->grow(n);
+    if (t.has_w) t.w.grow(n);
+    const int ntiles = ceil_div(n, kRadixTile);
+    sc.hist.grow(size_t(kRadixBins) * ntiles);
+    sc.tiles.grow(scan_tile_ints((long long)kRadixBins * ntiles, 1));
+    sc.grand.grow(8);
+    sc.lev.grow(kMaxDepth + 4);
+    sc.rcnt.grow(8);
+    t.off_sphere.grow(1);
+    // Cluster capacity per batch of speculatively enqueued levels: a level has at most 4x the
+    // clusters of the one above and at most 4 floor(n / (n0 + 1)) (splitting clusters hold
+    // > n0 particles each, disjointly); the batch stops at the depth a uniform distribution
+    // reaches (+1) or when the bound would pass `budget`.
+    const long long per_level = 4 * (n / (n0 + 1));
+    const long long budget = 6 + 2 * per_level + 4096;
+    int d_est = 0;
+    while (d_est < kMaxDepth && 6.0 * std::pow(4.0, d_est) * std::max(n0, 1) < double(n)) ++d_est;
+
+    LevelDesc* lev = reinterpret_cast<LevelDesc*>(sc.lev.p);
+    t.reserve_clusters(64, s);
+    reserve_quadrants(sc, t.cap, 0, s);
+    ClusterPtrs c = cluster_ptrs(t);
+    CSFS_CK(cudaMemsetAsync(t.off_sphere.p, 0, sizeof(int), s));
+    k_root_init<<<1, 32, 0, s>>>(c, sc.rcnt);
+    CSFS_LAUNCH_CHECK();
+    const int grun = std::max(1, ceil_div(n, (long long)kTile));
+    k_face_label<<<grun, kRunThreads, 0, s>>>(xyz, n, sc.fxi, sc.feta, sc.lab, t.off_sphere, sc.rcnt, t.bnd);
+    CSFS_LAUNCH_CHECK();
+    k_root_geom<<<1, 32, 0, s>>>(c, sc.rcnt, shrink, n0, lev, sc.scnt, sc.sbnd);
+    CSFS_LAUNCH_CHECK();
+    CSFS_CK(cudaMemcpyAsync(sc.host + kHostRoots, sc.rcnt.p, 6 * sizeof(int), cudaMemcpyDeviceToHost, s));
+
+    // ---- levels (cluster_tree.cpp:87-141), no host round trip inside a batch -------------
+    int d = 0;
+    long long frontier = 6, used = 6;  // exact at the start of a batch
+    const LevelDesc* hl = reinterpret_cast<const LevelDesc*>(sc.host + kHostLev);
+    for (;;) {
+        long long cap = used, fb = frontier;
+        int d_end = d;
+        std::vector<long long> fbound;  // frontier-size bound of each level of the batch
+        for (;;) {  // levels d .. d_end allocate children at depths d+1 .. d_end+1
+            const long long kids = std::min(4 * fb, per_level);
+            if (d_end > d && (cap + kids > budget || d_end > d_est)) {
+                --d_end;
+                break;
+            }
+            fbound.push_back(fb);
+            cap += kids;
+            fb = kids;
+            if (d_end + 1 >= kMaxDepth) break;
+            ++d_end;
+        }
+        if (d_end < d) d_end = d;
+        if (cap > INT_MAX / 16) throw std::invalid_argument("cluster tree too large");
+        t.ncl = int(used);  // reserve_clusters keeps the first t.ncl clusters
+        t.reserve_clusters(int(cap), s);
+        reserve_quadrants(sc, t.cap, int(used), s);
+        c = cluster_ptrs(t);
+        sc.cbase.grow(size_t(*std::max_element(fbound.begin(), fbound.end())));
+        for (int k = d; k <= d_end; ++k) {
+            k_label<<<grun, kRunThreads, 0, s>>>(n, k, lev, c, sc.fxi, sc.feta, sc.lab, sc.qchild, sc.scnt, sc.sbnd);
+            CSFS_LAUNCH_CHECK();
+            k_alloc_scan<<<1, kAllocThreads, 0, s>>>(k, lev, c, sc.scnt, sc.cbase, t.cap);
+            CSFS_LAUNCH_CHECK();
+            k_alloc_fill<<<ceil_div(4 * fbound[k - d], kThreads), kThreads, 0, s>>>(k, lev, c, sc.scnt, sc.scnt,
+                                                                                 sc.sbnd, sc.cbase, sc.qchild,
+                                                                                 shrink, n0);
+            CSFS_LAUNCH_CHECK();
+        }
+        CSFS_CK(cudaMemcpyAsync(sc.host + kHostLev, sc.lev.p, (d_end + 2) * sizeof(LevelDesc),
+                                cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaStreamSynchronize(s));
+        for (int k = d; k <= d_end + 1; ++k)
+            if (hl[k].ovf) throw std::runtime_error("cluster tree build: capacity bound violated");
+        const LevelDesc nx = hl[d_end + 1];
+        if (nx.nsplit == 0 || d_end + 1 >= kMaxDepth) {
+            for (int k = 0; k <= d_end + 1 && hl[k].cnt > 0; ++k) {
+                t.level_first.push_back(hl[k].first);
+                t.level_count.push_back(hl[k].cnt);
+                t.ncl = hl[k].first + hl[k].cnt;
+            }
+            break;
+        }
+        d = d_end + 1;
+        frontier = nx.cnt;
+        used = (long long)nx.first + nx.cnt;
+    }
+    t.root_count.assign(sc.host + kHostRoots, sc.host + kHostRoots + 6);
+
+    // ---- one stable sort by leaf: the reference's order ----------------------------------
+    const int gp = ceil_div(n, kThreads);
+    k_leaf_key<<<gp, kThreads, 0, s>>>(n, sc.lab, sc.qchild, t.begin, sc.key);
+    CSFS_LAUNCH_CHECK();
+    int bits = 1;
+    while (bits < 31 && (1LL << bits) < n) ++bits;
+    const int* sorted = radix_sort_positions(n, bits, sc.key, sc.kb, sc.vb, sc.sorted, sc.hist, sc.tiles, sc.grand, s);
+    k_gather_tree<<<gp, kThreads, 0, s>>>(n, sorted, sc.fxi, sc.feta, xyz, t.perm, t.xi, t.eta, t.px, t.py, t.pz);
+    CSFS_LAUNCH_CHECK();
+    finish_tree(t, w_in, n, cheb, s, w_ready);
 }
 
 void tree_proxy_radii(DeviceTree& t, cudaStream_t s) {
