@@ -127,14 +127,14 @@ std::unique_ptr<csfs_b200_ctx> new_context(int device) {
     CSFS_CK(cudaSetDevice(device));
     CSFS_CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
     {
-        // the upward pass runs on `aux` under the traversal: the lowest priority, so the
-        // latency-bound list kernels on the critical path get the SMs first
+        // the upward pass runs on `aux` under the list phase, which runs on `hi`: the
+        // latency-bound list kernels (the critical path) get the SMs first.  (The least
+        // priority is also the default one, so `aux` alone could not rank below the caller's
+        // stream.)
         int lo = 0, hi = 0;
         CSFS_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-#ifndef CSFS_AUX_PRIORITY_LOW
-#define CSFS_AUX_PRIORITY_LOW 1
-#endif
-        CSFS_CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, CSFS_AUX_PRIORITY_LOW ? lo : 0));
+        CSFS_CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo));
+        CSFS_CK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, hi));
     }
     CSFS_CK(cudaEventCreateWithFlags(&c->w_copied, cudaEventDisableTiming));
     for (auto& e : c->ev) CSFS_CK(cudaEventCreate(&e));
@@ -159,12 +159,14 @@ void free_context(csfs_b200_ctx* c) {
     cudaSetDevice(c->device);
     if (c->own) cudaStreamSynchronize(c->own);
     if (c->aux) cudaStreamSynchronize(c->aux);
+    if (c->hi) cudaStreamSynchronize(c->hi);
     if (c->comm) ncclCommDestroy(c->comm);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->sc.host) cudaFreeHost(c->sc.host);
     if (c->own) cudaStreamDestroy(c->own);
     if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->hi) cudaStreamDestroy(c->hi);
     if (c->w_copied) cudaEventDestroy(c->w_copied);
     delete c;
 }
@@ -263,12 +265,15 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     if (serial_up) CSFS_CK(cudaEventRecord(ev[1], s));
 
     static const bool trace = std::getenv("CSFS_B200_TRACE_LISTS") != nullptr;
-    dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
-    if (trace) CSFS_CK(cudaEventRecord(ev[8], s));
-    build_items(T, S, c->lists, c->items, c->sc, s);
-    if (trace) CSFS_CK(cudaEventRecord(ev[9], s));
-    prepare_mutual(c, s, true);
-    CSFS_CK(cudaEventRecord(ev[3], s));
+    cudaStream_t ls = c->hi;  // the list phase, forked from s at ev[1] and joined at ev[3]
+    CSFS_CK(cudaStreamWaitEvent(ls, ev[1], 0));
+    dual_traversal(T, S, f.mac, n0, c->lists, c->sc, ls);
+    if (trace) CSFS_CK(cudaEventRecord(ev[8], ls));
+    build_items(T, S, c->lists, c->items, c->sc, ls);
+    if (trace) CSFS_CK(cudaEventRecord(ev[9], ls));
+    prepare_mutual(c, ls, true);
+    CSFS_CK(cudaEventRecord(ev[3], ls));
+    CSFS_CK(cudaStreamWaitEvent(s, ev[3], 0));
     if (trace) {
         CSFS_CK(cudaEventSynchronize(ev[3]));
         fprintf(stderr, "lists: traversal %.3f items %.3f mutual %.3f ms\n", ev_ms(ev[1], ev[8]), ev_ms(ev[8], ev[9]),

@@ -21,6 +21,7 @@ struct csfs_b200_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t aux = nullptr;  // the upward pass, overlapped with the dual traversal
+    cudaStream_t hi = nullptr;   // the list phase (traversal, items, symmetric pairs): greatest priority
     cudaEvent_t w_copied = nullptr;  // host API: the weights' H2D copy (on aux) is done
     std::string err;
     csfs_b200::DeviceTree ttree, stree;
