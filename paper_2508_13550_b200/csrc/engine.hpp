@@ -165,6 +165,7 @@ struct Items {
     DevBuf<int4> mpair;
     DevBuf<long long> mpoff, mlist, unit_b;
     DevBuf<double> partial;
+    DevBuf<int> oitem, opair, ocnt, otiles;  // a rank's own items / pairs (interact.cu compact_owned)
     int n_mutual = 0;
     long long n_partial = 0;  // doubles
     unsigned long long skipped_pairs = 0;

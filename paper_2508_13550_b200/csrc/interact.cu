@@ -21,6 +21,7 @@
 
 #include "engine.hpp"
 #include "kernels_dev.cuh"
+#include "scan.cuh"
 
 namespace csfs_b200 {
 
@@ -96,6 +97,9 @@ struct InteractParams {
     double* out_q;  // proxy potentials (ncl_t x npp x dim)
     const int* anchor;  // per item owner key (nullptr: every item is ours)
     long long own_b, own_e;
+    // a rank's own items, compacted (interact(): partitioned calls): item idx[0 .. *n_own)
+    const int* idx;
+    const int* n_own;
     const double2* log_tab;  // kLogTabWords entries (fastmath.cuh)
     // symmetric-pair partial blocks of each item's key (k_mutual ran first), added to the
     // item's outputs in ascending block order; mcnt == nullptr: none
@@ -126,14 +130,16 @@ __global__ void __launch_bounds__(kIB, MinBlocksOf<Op>::value) k_interact(Intera
         __syncthreads();
         const int q = item_sh;
         __syncthreads();
-        if (q >= P.n_items) break;
+        const int n_items = P.n_own ? *P.n_own : P.n_items;
+        if (q >= n_items) break;
 #ifndef CSFS_ITEM_ORDER_REVERSED
 #define CSFS_ITEM_ORDER_REVERSED 1
 #endif
         // the queue hands out the items back to front: cluster items (CP/CC, the largest,
         // up to ~1.3M evaluations each at C5) first, the uniform leaf items last, so the
         // kernel's tail is made of short items (longest-first scheduling)
-        const int it = CSFS_ITEM_ORDER_REVERSED ? P.n_items - 1 - q : q;
+        const int iq = CSFS_ITEM_ORDER_REVERSED ? n_items - 1 - q : q;
+        const int it = P.idx ? P.idx[iq] : iq;
         if (P.anchor) {
             const int a = P.anchor[it];
             if (a >= 0 && (a < P.own_b || a >= P.own_e)) continue;  // another rank's target
@@ -320,6 +326,8 @@ struct MutualParams {
     double* partial;
     const double2* log_tab;
     long long own_b, own_e;
+    const int* idx;    // a rank's own pairs, compacted: pair idx[0 .. *n_own)
+    const int* n_own;
 };
 
 // double butterfly shuffle as two explicit 32-bit halves in one asm block (keeps the halves in place; the
@@ -349,9 +357,10 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
     for (;;) {
         if (tid == 0) pair_sh = atomicAdd(P.counter, 1);
         __syncthreads();  // also: the previous pair's shared-memory reads are done
-        const int p = pair_sh;
+        const int pq = pair_sh;
         __syncthreads();
-        if (p >= P.n_pairs) break;
+        if (pq >= (P.n_own ? *P.n_own : P.n_pairs)) break;
+        const int p = P.idx ? P.idx[pq] : pq;
         if (P.anchor) {
             const long long a = P.anchor[p];
             if (a >= 0 && (a < P.own_b || a >= P.own_e)) continue;  // CTA-uniform
@@ -561,6 +570,26 @@ void launch_mutual(const MutualParams& m, const Op& op, cudaStream_t s) {
     }
 }
 
+// Stable compaction of the work entries a rank owns (anchor < 0: every rank; else the
+// anchor particle in [b, e)): idx[0 .. *count).  A partitioned call then only dequeues its
+// own items instead of skipping the other ranks' ones one queue step at a time (a fixed
+// ~1.4 ms per rank at C5, 14% of the evaluation at 8 ranks).
+void compact_owned(const int* anchor, int n, Own own, DevBuf<int>& idx, int* count, DevBuf<int>& tiles,
+                   cudaStream_t s) {
+    idx.grow(std::max(n, 1));
+    tiles.grow(scan_tile_ints(n, 1));
+    int* out = idx.p;
+    const long long b = own.b, e = own.e;
+    auto f = [=] __device__(long long i, int* c) {
+        const int a = anchor[i];
+        c[0] = (a < 0 || (a >= b && a < e)) ? 1 : 0;
+    };
+    auto em = [=] __device__(long long i, const int* c, const int* pre) {
+        if (c[0]) out[pre[0]] = int(i);
+    };
+    run_scan<1>(n, f, em, tiles.p, count, s);
+}
+
 }  // namespace
 
 void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, Items& items,
@@ -618,6 +647,19 @@ void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src,
         p.moff = items.moff;
         p.mlist = items.mlist;
         p.partial = items.partial;
+    }
+    if (!everything) {
+        items.ocnt.grow(2);
+        compact_owned(items.anchor, items.n_items, own, items.oitem, items.ocnt.p, items.otiles, s);
+        p.idx = items.oitem;
+        p.n_own = items.ocnt.p;
+        p.anchor = nullptr;
+        if (items.mutual) {
+            compact_owned(items.manchor, items.n_mutual, own, items.opair, items.ocnt.p + 1, items.otiles, s);
+            m.idx = items.opair;
+            m.n_own = items.ocnt.p + 1;
+            m.anchor = nullptr;
+        }
     }
     with_op(k, [&](auto op) {
         if (items.mutual) launch_mutual(m, op, s);

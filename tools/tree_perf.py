@@ -1,6 +1,6 @@
-"""Tree-build phase time of one config, both builds (label-then-sort default and the
-level-synchronous CSFS_B200_TREE=levels), from SumStats over repeated calls:
-python tools/tree_perf.py [config] [reps]"""
+"""Phase times (SumStats, median over repeated calls) of one config, with both tree builds
+(label-then-sort default and the level-synchronous CSFS_B200_TREE=levels; TREE_MODES=sort
+for the default only): python tools/tree_perf.py [config] [reps]"""
 import os
 import statistics
 import sys
@@ -15,17 +15,19 @@ eng = Engine(0)
 p = ParticleSet(wl.xyz, wl.weights)
 cfg = TraversalConfig(mac=wl.mac, degree=wl.degree, n0=wl.n0)
 k = Kernel.parse(wl.kernel)
-for mode in ("", "levels", ""):
+modes = ["" if m == "sort" else m for m in os.environ.get("TREE_MODES", "sort,levels,sort").split(",")]
+for mode in modes:
     if mode:
         os.environ["CSFS_B200_TREE"] = mode
     else:
         os.environ.pop("CSFS_B200_TREE", None)
-    tb, tl, tt = [], [], []
+    ph = {f: [] for f in ("t_tree_build", "t_upward", "t_lists", "t_interact", "t_downward", "t_total")}
     for _ in range(reps):
         st = SumStats()
         eng.csfmm_sum(p, p, k, cfg, st)
-        tb.append(st.t_tree_build * 1e3)
-        tl.append(st.t_lists * 1e3)
-        tt.append(st.t_total * 1e3)
-    print(f"{name} tree={mode or 'sort':7s} build {statistics.median(tb):.3f} ms (min {min(tb):.3f}) "
-          f"lists {statistics.median(tl):.3f} total {statistics.median(tt):.3f}")
+        for f in ph:
+            ph[f].append(getattr(st, f) * 1e3)
+    med = {f: statistics.median(v) for f, v in ph.items()}
+    print(f"{name} tree={mode or 'sort':7s} build {med['t_tree_build']:.3f} ms (min {min(ph['t_tree_build']):.3f}) "
+          f"upward {med['t_upward']:.3f} lists {med['t_lists']:.3f} interact {med['t_interact']:.3f} "
+          f"downward {med['t_downward']:.3f} total {med['t_total']:.3f}")
