@@ -5,6 +5,7 @@
 //   from CUDA events (the reference's steady_clock SumStats, summation.cpp:407-419).
 // There is no CPU fallback: without a usable sm_100a device every call fails.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -182,7 +183,7 @@ void prepare_mutual(csfs_b200_ctx* c, cudaStream_t s, bool global) {
     if (!c->shared || !c->use_mutual || c->kspec.out_dim() != 1) return;
     std::vector<long long> ub, ue;
     if (global && !c->mutual_unit_scope) ub.push_back(0);
-    else partition_units(c->ttree, ub, ue);
+    else partition_units(c->ttree, ub, ue, s);
     build_mutual(c->ttree, c->items, ub, c->sc, s);
     c->items.mutual = c->items.n_partial > 0;
 }
@@ -298,7 +299,7 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
 }
 
 void part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz, const double* sw, size_t ns,
-               const KernelSpec& ks, const FmmConfig& f, cudaStream_t s) {
+               const KernelSpec& ks, const FmmConfig& f, cudaStream_t s, bool early_upward) {
     validate(f, nt, ns);
     c->have_state = false;
     c->have_src_tree = false;
@@ -312,37 +313,77 @@ void part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     c->dim = ks.out_dim();
     c->cheb = make_cheb(f.degree);
     const int n0 = f.resolved_n0();
+    static const bool trace = std::getenv("CSFS_B200_TRACE_PLAN") != nullptr;
+    std::vector<std::pair<const char*, double>> marks;
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        CSFS_CK(cudaDeviceSynchronize());
+        marks.push_back({what, std::chrono::duration<double, std::milli>(
+                                   std::chrono::steady_clock::now().time_since_epoch()).count()});
+    };
+    mark("start");
     c->shared = (nt == ns) && device_equal(txyz, sxyz, nt * 3 * sizeof(double), c->sc, s);
     DeviceTree& T = c->ttree;
     DeviceTree& S = c->shared ? c->ttree : c->stree;
     build_tree(T, c->sc, txyz, c->shared ? sw : nullptr, (long long)nt, f.degree, n0, f.shrink, c->cheb, s);
     if (!c->shared) build_tree(S, c->sc, sxyz, sw, (long long)ns, f.degree, n0, f.shrink, c->cheb, s);
-    dual_traversal(T, S, f.mac, n0, c->lists, c->sc, s);
-    build_items(T, S, c->lists, c->items, c->sc, s);
-    prepare_mutual(c, s, false);  // unit scope: the same pairs for every rank count
+    mark("trees");
     // partition units: depth-1 subtrees plus unsplit roots, in tree order
     for (int w = 0; w < 2; ++w) {
         const DeviceTree& t = (w == 0 || c->shared) ? T : S;
-        partition_units(t, c->unit_b[w], c->unit_e[w]);
+        partition_units(t, c->unit_b[w], c->unit_e[w], s);
         c->unit_cost[w].assign(c->unit_b[w].size(), 0.0);
         if (w == 1)
             for (size_t i = 0; i < c->unit_b[1].size(); ++i)
                 c->unit_cost[1][i] = double(c->unit_e[1][i] - c->unit_b[1][i]);
     }
+    if (early_upward) {  // sources split by particle count: known now
+        const int R = c->nranks;
+        const auto srun = split_contiguous(c->unit_cost[1], R);
+        c->s_range.assign(2 * R, 0);
+        for (int r = 0; r < R; ++r)
+            if (srun[r].second > srun[r].first) {
+                c->s_range[2 * r] = c->unit_b[1][srun[r].first];
+                c->s_range[2 * r + 1] = c->unit_e[1][srun[r].second - 1];
+            }
+        CSFS_CK(cudaEventRecord(c->ev[10], s));
+        CSFS_CK(cudaStreamWaitEvent(c->aux, c->ev[10], 0));
+        upward_pass(S, c->cheb, c->aux, 1, Own{c->s_range[2 * c->rank], c->s_range[2 * c->rank + 1]});
+        CSFS_CK(cudaEventRecord(c->ev[11], c->aux));
+        exchange_order(c, S, s);  // host work while the upward pass runs
+    }
+    mark("units+upward+order");
+    // the list phase on the greatest-priority stream (as in run_csfmm)
+    cudaStream_t ls = c->hi;
+    CSFS_CK(cudaEventRecord(c->ev[10], s));
+    CSFS_CK(cudaStreamWaitEvent(ls, c->ev[10], 0));
+    dual_traversal(T, S, f.mac, n0, c->lists, c->sc, ls);
+    mark("traversal");
+    build_items(T, S, c->lists, c->items, c->sc, ls);
+    mark("items");
+    prepare_mutual(c, ls, false);  // unit scope: the same pairs for every rank count
+    mark("mutual");
     {
-        const int ni = c->items.n_items;
-        std::vector<int> anchor(ni);
-        std::vector<double> cost(ni);
-        if (ni) {
-            CSFS_CK(cudaMemcpy(anchor.data(), c->items.anchor.p, ni * sizeof(int), cudaMemcpyDeviceToHost));
-            CSFS_CK(cudaMemcpy(cost.data(), c->items.cost.p, ni * sizeof(double), cudaMemcpyDeviceToHost));
-        }
-        const auto& ub = c->unit_b[0];
-        for (int i = 0; i < ni; ++i) {
-            if (anchor[i] < 0) continue;
-            const size_t u = size_t(std::upper_bound(ub.begin(), ub.end(), (long long)anchor[i]) - ub.begin()) - 1;
-            c->unit_cost[0][u] += cost[i];
-        }
+        // target units' costs: the pair evaluations of their items, summed on the device in
+        // exact integer arithmetic (every rank must derive the same split)
+        const int ni = c->items.n_items, nu = int(c->unit_b[0].size());
+        c->ubeg.grow(std::max(nu, 1));
+        c->ucost.grow(std::max(nu, 1));
+        CSFS_CK(cudaMemcpyAsync(c->ubeg.p, c->unit_b[0].data(), nu * sizeof(long long), cudaMemcpyHostToDevice, ls));
+        CSFS_CK(cudaMemsetAsync(c->ucost.p, 0, std::max(nu, 1) * sizeof(unsigned long long), ls));
+        unit_costs(c->items, ni, c->ubeg.p, nu, c->ucost.p, ls);
+        std::vector<unsigned long long> uc(std::max(nu, 1));
+        CSFS_CK(cudaMemcpyAsync(uc.data(), c->ucost.p, std::max(nu, 1) * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, ls));
+        CSFS_CK(cudaStreamSynchronize(ls));
+        for (int u = 0; u < nu; ++u) c->unit_cost[0][u] = double(uc[u]);
+    }
+    CSFS_CK(cudaEventRecord(c->ev[10], ls));  // the lists are ready for work on s
+    CSFS_CK(cudaStreamWaitEvent(s, c->ev[10], 0));
+    mark("costs");
+    if (trace) {
+        for (size_t i = 1; i < marks.size(); ++i)
+            fprintf(stderr, "plan %s %.3f ms\n", marks[i].first, marks[i].second - marks[i - 1].second);
     }
     c->part_planned = true;
 }

@@ -68,6 +68,8 @@ struct csfs_b200_ctx {
     csfs_b200::DevBuf<double> xq;      // proxy-weight exchange buffer, owner-packed
     csfs_b200::DevBuf<int> xidx;       // source clusters in exchange order (rank by rank)
     csfs_b200::DevBuf<unsigned long long> xcount;  // executed evaluations of the owned items
+    csfs_b200::DevBuf<long long> ubeg;             // partition units' first particles (device)
+    csfs_b200::DevBuf<unsigned long long> ucost;   // per unit: pair evaluations of its items
     std::vector<long long> xq_off;     // per rank: first cluster of its segment in xidx (+ end)
     std::vector<long long> t_range, s_range;  // per rank: owned tree-order [b, e) x 2
     double t_exchange = 0.0;           // last call: seconds in the two exchanges (rank 0)
@@ -118,8 +120,11 @@ void run_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
                cudaEvent_t w_ready = nullptr);
 // The partition plan of one rank (full trees, lists, items with unit-scope symmetric
 // pairs, partition units and their costs) — csfs_b200_part_plan.
+// early_upward (the group rank program): the rank's source split (by particle count) is
+// known once the trees are built, so its upward pass starts then on the aux stream, under
+// the traversal; c->ev[11] marks its end and c->s_range holds every rank's sources.
 void part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sxyz, const double* sw, size_t ns,
-               const KernelSpec& ks, const FmmConfig& f, cudaStream_t s);
+               const KernelSpec& ks, const FmmConfig& f, cudaStream_t s, bool early_upward = false);
 void fill_stats(csfs_b200_ctx* c, csfs_b200_stats* st);
 
 }  // namespace capi
@@ -134,5 +139,7 @@ void run_csfmm_group(csfs_b200_ctx* c, const double* txyz, size_t nt, const doub
 // cost (distributed.py split_contiguous restated): the cut k sits at the unit boundary
 // whose prefix cost is closest to k*total/world, never moving backwards.
 std::vector<std::pair<int, int>> split_contiguous(const std::vector<double>& costs, int world);
+// partition.cu: exchange order of the owned source clusters (needs c->s_range)
+void exchange_order(csfs_b200_ctx* c, const DeviceTree& S, cudaStream_t s);
 
 }  // namespace csfs_b200

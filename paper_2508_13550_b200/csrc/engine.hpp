@@ -224,7 +224,10 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& list
 void build_mutual(const DeviceTree& tgt, Items& items, const std::vector<long long>& unit_begins, Scratch& sc,
                   cudaStream_t s);
 // Partition units of a tree: (begin, end) particle ranges in tree order.
-void partition_units(const DeviceTree& t, std::vector<long long>& b, std::vector<long long>& e);
+void partition_units(const DeviceTree& t, std::vector<long long>& b, std::vector<long long>& e, cudaStream_t s);
+// Pair evaluations of the items anchored in each unit (ubeg: the units' first particles).
+void unit_costs(const Items& it, int n_items, const long long* ubeg, int nu, unsigned long long* ucost,
+                cudaStream_t s);
 
 // interact.cu
 void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, Items& items,

@@ -151,6 +151,43 @@ Inputs share_inputs(Ctx* c, const Inputs& in0, bool same_xyz, cudaStream_t s) {
     return in;
 }
 
+}  // namespace
+
+// Exchange order of the proxy weights: the owned source clusters (depth >= 1) of rank 0,
+// rank 1, ... (c->xidx on the device, c->xq_off per rank); c->s_range must be set.
+void exchange_order(csfs_b200_ctx* c, const DeviceTree& S, cudaStream_t s) {
+    const int R = c->nranks;
+    std::vector<int> beg(S.ncl), dep(S.ncl);
+    CSFS_CK(cudaMemcpyAsync(beg.data(), S.begin.p, S.ncl * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaMemcpyAsync(dep.data(), S.depth.p, S.ncl * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaStreamSynchronize(s));
+    // owner of each depth >= 1 cluster (its first particle's rank range), then a counting
+    // sort by owner that keeps cluster order inside each rank: O(ncl)
+    std::vector<int> owner(S.ncl, -1);
+    c->xq_off.assign(R + 1, 0);
+    for (int i = 0; i < S.ncl; ++i) {
+        if (dep[i] < 1) continue;
+        for (int r = 0; r < R; ++r)
+            if (beg[i] >= c->s_range[2 * r] && beg[i] < c->s_range[2 * r + 1]) {
+                owner[i] = r;
+                ++c->xq_off[r + 1];
+                break;
+            }
+    }
+    for (int r = 0; r < R; ++r) c->xq_off[r + 1] += c->xq_off[r];
+    std::vector<int> idx(size_t(c->xq_off[R]));
+    std::vector<long long> at(c->xq_off.begin(), c->xq_off.end() - 1);
+    for (int i = 0; i < S.ncl; ++i)
+        if (owner[i] >= 0) idx[size_t(at[owner[i]]++)] = i;
+    const long long n = (long long)idx.size();
+    c->xidx.grow(std::max<long long>(n, 1));
+    c->xq.grow(size_t(std::max<long long>(n, 1)) * S.npp);
+    if (n) CSFS_CK(cudaMemcpyAsync(c->xidx.p, idx.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
+    CSFS_CK(cudaStreamSynchronize(s));  // idx's lifetime
+}
+
+namespace {
+
 std::pair<long long, long long> owned_range(const std::vector<long long>& b, const std::vector<long long>& e,
                                             std::pair<int, int> run) {
     if (run.second <= run.first) return {0, 0};
@@ -161,43 +198,20 @@ std::pair<long long, long long> owned_range(const std::vector<long long>& b, con
 void phase_plan(Ctx* c, const Inputs& in, const KernelSpec& ks, const FmmConfig& f, cudaStream_t s) {
     cudaEvent_t* ev = c->ev;
     CSFS_CK(cudaEventRecord(ev[0], s));
-    capi::part_plan(c, in.txyz, in.nt, in.sxyz, in.sw, in.ns, ks, f, s);
+    // the owned upward pass starts inside the plan, under the traversal (part_plan early_upward)
+    capi::part_plan(c, in.txyz, in.nt, in.sxyz, in.sw, in.ns, ks, f, s, true);
     CSFS_CK(cudaEventRecord(ev[1], s));
     const int R = c->nranks;
     const auto trun = split_contiguous(c->unit_cost[0], R);
-    const auto srun = split_contiguous(c->unit_cost[1], R);
     c->t_range.assign(2 * R, 0);
-    c->s_range.assign(2 * R, 0);
     for (int r = 0; r < R; ++r) {
         const auto t = owned_range(c->unit_b[0], c->unit_e[0], trun[r]);
-        const auto q = owned_range(c->unit_b[1], c->unit_e[1], srun[r]);
         c->t_range[2 * r] = t.first;
         c->t_range[2 * r + 1] = t.second;
-        c->s_range[2 * r] = q.first;
-        c->s_range[2 * r + 1] = q.second;
     }
     DeviceTree& S = c->shared ? c->ttree : c->stree;
-    const Own own_s{c->s_range[2 * c->rank], c->s_range[2 * c->rank + 1]};
-    upward_pass(S, c->cheb, s, 1, own_s);
-    // exchange order: the owned source clusters (depth >= 1) of rank 0, rank 1, ...
-    std::vector<int> beg(S.ncl), dep(S.ncl);
-    CSFS_CK(cudaMemcpyAsync(beg.data(), S.begin.p, S.ncl * sizeof(int), cudaMemcpyDeviceToHost, s));
-    CSFS_CK(cudaMemcpyAsync(dep.data(), S.depth.p, S.ncl * sizeof(int), cudaMemcpyDeviceToHost, s));
-    CSFS_CK(cudaStreamSynchronize(s));
-    std::vector<int> idx;
-    idx.reserve(S.ncl);
-    c->xq_off.assign(R + 1, 0);
-    for (int r = 0; r < R; ++r) {
-        c->xq_off[r] = (long long)idx.size();
-        const long long b = c->s_range[2 * r], e = c->s_range[2 * r + 1];
-        for (int i = 0; i < S.ncl; ++i)
-            if (dep[i] >= 1 && beg[i] >= b && beg[i] < e) idx.push_back(i);
-    }
-    c->xq_off[R] = (long long)idx.size();
-    const long long n = (long long)idx.size();
-    c->xidx.grow(std::max<long long>(n, 1));
-    c->xq.grow(size_t(std::max<long long>(n, 1)) * S.npp);
-    if (n) CSFS_CK(cudaMemcpyAsync(c->xidx.p, idx.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
+    CSFS_CK(cudaStreamWaitEvent(s, ev[11], 0));  // the owned upward pass (aux)
+    // c->xidx / c->xq_off: the exchange order, set by part_plan (exchange_order)
     const long long ob = c->xq_off[c->rank], on = c->xq_off[c->rank + 1] - ob;
     if (on) {
         k_pack<<<ceil_div(on * S.npp, kTB), kTB, 0, s>>>(c->xidx.p + ob, on, S.npp, S.qw.p, c->xq.p + ob * S.npp);

@@ -357,13 +357,44 @@ __global__ void __launch_bounds__(256) k_traverse_step(const TreeView T, const T
 
 }  // namespace
 
-void partition_units(const DeviceTree& t, std::vector<long long>& ub, std::vector<long long>& ue) {
+namespace {
+// Each item's pair evaluations into its target unit (the last unit beginning at or before
+// its anchor); u64 atomics: exact, so the sum is order independent.
+__global__ void k_unit_costs(int n_items, const int* __restrict__ anchor, const double* __restrict__ cost,
+                             const long long* __restrict__ ubeg, int nu, unsigned long long* ucost) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int u = -1;
+    unsigned long long v = 0;
+    if (i < n_items && anchor[i] >= 0) {
+        int lo = 0, hi = nu;  // first unit with ubeg > anchor
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if (ubeg[m] <= anchor[i]) lo = m + 1;
+            else hi = m;
+        }
+        u = lo - 1;
+        v = (unsigned long long)cost[i];
+    }
+    if (u >= 0) atomicAdd(&ucost[u], v);
+}
+}  // namespace
+
+void unit_costs(const Items& it, int n_items, const long long* ubeg, int nu, unsigned long long* ucost,
+                cudaStream_t s) {
+    if (n_items <= 0 || nu <= 0) return;
+    k_unit_costs<<<ceil_div(n_items, 256), 256, 0, s>>>(n_items, it.anchor, it.cost, ubeg, nu, ucost);
+    CSFS_LAUNCH_CHECK();
+}
+
+void partition_units(const DeviceTree& t, std::vector<long long>& ub, std::vector<long long>& ue, cudaStream_t s) {
     const int nfirst = t.depth_max() >= 1 ? t.level_first[1] + t.level_count[1] : 6;
     std::vector<int> b(nfirst), e(nfirst), nch(nfirst), dep(nfirst);
-    CSFS_CK(cudaMemcpy(b.data(), t.begin.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
-    CSFS_CK(cudaMemcpy(e.data(), t.end.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
-    CSFS_CK(cudaMemcpy(nch.data(), t.nchild.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
-    CSFS_CK(cudaMemcpy(dep.data(), t.depth.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost));
+    // on the stream that built the tree (the legacy default stream does not order with it)
+    CSFS_CK(cudaMemcpyAsync(b.data(), t.begin.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaMemcpyAsync(e.data(), t.end.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaMemcpyAsync(nch.data(), t.nchild.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaMemcpyAsync(dep.data(), t.depth.p, nfirst * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CSFS_CK(cudaStreamSynchronize(s));
     std::vector<std::pair<long long, long long>> u;
     for (int i = 0; i < nfirst; ++i)
         if (e[i] > b[i] && (dep[i] == 1 || nch[i] == 0)) u.push_back({b[i], e[i]});

@@ -598,7 +598,10 @@ __device__ __forceinline__ unsigned long long redux_max_u64(unsigned m, unsigned
 // share one slot (the top levels on coherent inputs) is reduced over the CTA and issues one
 // set of atomics; otherwise the lanes whose last runs share a slot combine them
 // (match_any + redux) and one of them issues the atomics.
-constexpr int kRun = 8;
+#ifndef CSFS_TREE_RUN
+#define CSFS_TREE_RUN 8
+#endif
+constexpr int kRun = CSFS_TREE_RUN;
 constexpr int kRunThreads = 256;
 constexpr int kTile = kRun * kRunThreads;
 constexpr int kTilePad = kTile + kTile / kRun;
