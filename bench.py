@@ -437,8 +437,10 @@ def run_ours(args, rt=None, engine_factory=None, clock_factory=None, fp64_peak=N
     if world == 1:
         # the HBM-type phases against the measured copy bandwidth (SURVEY.md §8d algorithmic
         # bytes): tree build = xyz in (24 B/pt) + per level xi, eta, idx moved (2 x 20 B/pt) +
-        # sorted xyz, w, perm out (36 B/pt); upward leaf = 24 B/pt + (p+1)^2 x 8 B per leaf;
-        # downward leaf = 16 B/pt + 8 dim B/pt
+        # sorted xyz, w, perm out (36 B/pt) — the traffic of the level-by-level partition;
+        # the label-then-sort build (tree.cu) moves 24 B/pt per level plus one sort and
+        # gather, i.e. about as much, so the same figure is kept; upward leaf = 24 B/pt +
+        # (p+1)^2 x 8 B per leaf; downward leaf = 16 B/pt + 8 dim B/pt
         n, npp = wl.n, (wl.degree + 1) ** 2
         hbm_bytes = {"t_tree_build": n * (24 + 40 * s0.tgt_depth + 36),
                      "t_upward": n * 24 + npp * 8 * s0.src_leaves,
