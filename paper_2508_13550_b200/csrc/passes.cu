@@ -89,6 +89,74 @@ __global__ void __launch_bounds__(kPassThreads)
     }
 }
 
+// Leaf P2M with register blocking (the default for compile-time degrees): the bases of a
+// chunk of 128 particles are staged as above; then thread (s, k1) — S particle subsets x
+// NP rows — accumulates the whole row k1 (NP outputs in registers) over the particles
+// j = s, s + S, ...: per particle one shared load of w Lx[k1] and NP/2 two-wide loads of
+// the particle's Ly row (shared by the NP threads of subset s) for NP FMAs, instead of two
+// shared loads per FMA.  The S partial rows are added in fixed subset order at the end
+// (deterministic; roundoff-level difference from the reference's serial sum, within the
+// 1e-12 proxy-weight bar).
+template <int NP>
+__global__ void __launch_bounds__(kPassThreads)
+    k_p2m_rb(TreeView t, Cheb cheb, const double* __restrict__ w, double* __restrict__ qw, int mode, Own own) {
+    constexpr int S = kPassThreads / NP;  // particle subsets
+    constexpr int LDY = NP + 1;           // Ly row stride: 16-byte aligned pairs
+    constexpr int NPP = NP * NP;
+    __shared__ double WL[kP2mChunk * NP];
+    __shared__ __align__(16) double LY[kP2mChunk * LDY];
+    __shared__ double red[S * NPP];
+    const int c = blockIdx.x;
+    if (t.nchild[c] > 0 || !selected(t, c, mode, own)) return;
+    const int b = t.begin[c], e = t.end[c];
+    const double x0 = t.xi0[c], x1 = t.xi1[c], e0 = t.eta0[c], e1 = t.eta1[c];
+    const double xm = __dmul_rn(0.5, __dadd_rn(x0, x1)), xh = __dmul_rn(0.5, __dsub_rn(x1, x0));
+    const double em = __dmul_rn(0.5, __dadd_rn(e0, e1)), eh = __dmul_rn(0.5, __dsub_rn(e1, e0));
+    const int sub = threadIdx.x / NP, k1 = threadIdx.x - sub * NP;
+    const bool row = sub < S;
+    double acc[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) acc[k] = 0.0;
+    for (int base = b; base < e; base += kP2mChunk) {
+        const int m = min(kP2mChunk, e - base);
+        for (int j = threadIdx.x; j < m; j += kPassThreads) {  // one particle per thread
+            double lx[NP], ly[NP];
+            bary1d_fast<NP>(cheb, ref_coord(t.xi[base + j], xm, xh), lx);
+            bary1d_fast<NP>(cheb, ref_coord(t.eta[base + j], em, eh), ly);
+            const double wt = w[base + j];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                WL[j * NP + k] = __dmul_rn(wt, lx[k]);
+                LY[j * LDY + k] = ly[k];
+            }
+        }
+        __syncthreads();
+        if (row)
+            for (int j = sub; j < m; j += S) {
+                const double a = WL[j * NP + k1];
+                const double2* y2 = reinterpret_cast<const double2*>(LY + j * LDY);
+#pragma unroll
+                for (int k = 0; k + 1 < NP; k += 2) {
+                    const double2 v = y2[k >> 1];
+                    acc[k] = fma(a, v.x, acc[k]);
+                    acc[k + 1] = fma(a, v.y, acc[k + 1]);
+                }
+                if (NP & 1) acc[NP - 1] = fma(a, LY[j * LDY + NP - 1], acc[NP - 1]);
+            }
+        __syncthreads();
+    }
+    if (row)
+#pragma unroll
+        for (int k = 0; k < NP; ++k) red[sub * NPP + k1 * NP + k] = acc[k];
+    __syncthreads();
+    for (int o = threadIdx.x; o < NPP; o += kPassThreads) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < S; ++q) v += red[q * NPP + o];
+        qw[(long long)c * NPP + o] = v;
+    }
+}
+
 // The same leaf P2M on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64): per leaf the
 // proxy weights are the GEMM  pw = (w Lx)^T Ly  over its particles, (np x m) (m x np),
 // padded to 8 x 8 output tiles (np <= 8: one tile; np <= 16: 2 x 2, one warp each), K in
@@ -222,6 +290,64 @@ __global__ void __launch_bounds__(kPassThreads)
     for (int o = threadIdx.x; o < npp; o += kPassThreads, ++idx) qw[(long long)c * npp + o] = acc[idx];
 }
 
+// The same M2M with the (up to) four children in parallel: thread group q (kPassThreads
+// threads) builds child q's transfer matrices and its contribution Axi cw Aeta^T into
+// shared memory; the contributions are then added in child order — the same operations
+// and order as k_m2m, bit for bit, with 3 barriers per cluster instead of 12.  Used while
+// 16 (p+1)^2 doubles fit the 48 KB static window (degree <= 18).
+constexpr int kM2mGroups = 4;
+__global__ void __launch_bounds__(kM2mGroups * kPassThreads)
+    k_m2m4(TreeView t, Cheb cheb, int first, double* __restrict__ qw, int mode, Own own) {
+    extern __shared__ double sm[];
+    const int c = first + blockIdx.x;
+    const int nch = t.nchild[c];
+    if (nch == 0 || !selected(t, c, mode, own)) return;
+    const int np = cheb.np, npp = np * np;
+    const int q = threadIdx.x / kPassThreads, lt = threadIdx.x - q * kPassThreads;
+    double* Ax = sm + q * 3 * npp;  // At layout
+    double* Ae = Ax + npp;
+    double* tmp = Ae + npp;  // tmp[k1*np + m2]
+    double* contrib = sm + kM2mGroups * 3 * npp;
+    double pxm, pxh, pem, peh;
+    mid_half(t.xi0[c], t.xi1[c], pxm, pxh);
+    mid_half(t.eta0[c], t.eta1[c], pem, peh);
+    const int4 ch4 = t.child[c];
+    const int chs[4] = {ch4.x, ch4.y, ch4.z, ch4.w};
+    const bool mine = q < nch;
+    const int ch = mine ? chs[q] : 0;
+    if (mine) {
+        double cxm, cxh, cem, ceh;
+        mid_half(t.xi0[ch], t.xi1[ch], cxm, cxh);
+        mid_half(t.eta0[ch], t.eta1[ch], cem, ceh);
+        if (lt < np) transfer_cols(cheb, pxm, pxh, cxm, cxh, lt, Ax);
+        else if (lt < 2 * np) transfer_cols(cheb, pem, peh, cem, ceh, lt - np, Ae);
+    }
+    __syncthreads();
+    if (mine) {
+        const double* cw = qw + (long long)ch * npp;
+        for (int o = lt; o < npp; o += kPassThreads) {
+            const int k1 = o / np, m2 = o % np;
+            double s = 0.0;
+            for (int m1 = 0; m1 < np; ++m1) s = __dadd_rn(s, __dmul_rn(Ax[m1 * np + k1], cw[m1 * np + m2]));
+            tmp[o] = s;
+        }
+    }
+    __syncthreads();
+    if (mine)
+        for (int o = lt; o < npp; o += kPassThreads) {
+            const int k1 = o / np, k2 = o % np;
+            double s = 0.0;
+            for (int m2 = 0; m2 < np; ++m2) s = __dadd_rn(s, __dmul_rn(tmp[k1 * np + m2], Ae[m2 * np + k2]));
+            contrib[q * npp + o] = s;
+        }
+    __syncthreads();
+    for (int o = threadIdx.x; o < npp; o += kM2mGroups * kPassThreads) {
+        double acc = 0.0;
+        for (int k = 0; k < nch; ++k) acc = __dadd_rn(acc, contrib[k * npp + o]);
+        qw[(long long)c * npp + o] = acc;
+    }
+}
+
 // L2L (cluster_tree.cpp:256-279), one CTA per child at level `first..`:
 // child[n1,n2,d] += sum_{m1,m2} Axi[m1,n1] Aeta[m2,n2] P[m1,m2,d], done separably.
 __global__ void __launch_bounds__(kPassThreads)
@@ -341,23 +467,29 @@ void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s, int mode, Ow
     const int n_p2m = mode == 2 ? src.level_count[0] : src.ncl;  // depth 0 = ids 0..5
     auto p2m = [&](auto kern) { kern<<<n_p2m, kPassThreads, sm_p2m, s>>>(v, cheb, src.w, src.qw, mode, own); };
     auto p2m_tc = [&](auto kern) { kern<<<n_p2m, kPassThreads, 0, s>>>(v, cheb, src.w, src.qw, mode, own); };
-    static const bool dmma = [] {
-        const char* e = std::getenv("CSFS_B200_P2M");
-        return e && std::string(e) == "dmma";
-    }();
+    // CSFS_B200_P2M: unset = register-blocked FMA kernel, "fma" = the round-1/2 FMA kernel
+    // (two shared loads per FMA), "dmma" = FP64 tensor cores (DESIGN.md §3 A/B)
+    const char* pe = std::getenv("CSFS_B200_P2M");
+    const std::string pv = pe ? pe : "";
+    const bool dmma = pv == "dmma", plain = pv == "fma";
     switch (np) {
-        case 7: dmma ? p2m_tc(k_p2m_dmma<7>) : p2m(k_p2m<7>); break;
-        case 9: dmma ? p2m_tc(k_p2m_dmma<9>) : p2m(k_p2m<9>); break;
-        case 11: dmma ? p2m_tc(k_p2m_dmma<11>) : p2m(k_p2m<11>); break;
+        case 7: dmma ? p2m_tc(k_p2m_dmma<7>) : plain ? p2m(k_p2m<7>) : p2m_tc(k_p2m_rb<7>); break;
+        case 9: dmma ? p2m_tc(k_p2m_dmma<9>) : plain ? p2m(k_p2m<9>) : p2m_tc(k_p2m_rb<9>); break;
+        case 11: dmma ? p2m_tc(k_p2m_dmma<11>) : plain ? p2m(k_p2m<11>) : p2m_tc(k_p2m_rb<11>); break;
         default: p2m(k_p2m<0>);
     }
     CSFS_LAUNCH_CHECK();
     const size_t sm_m2m = size_t(3) * npp * sizeof(double);
+    const size_t sm_m2m4 = size_t(4 * kM2mGroups) * npp * sizeof(double);
     const int lo = mode == 1 ? 1 : 0;
     const int hi = mode == 2 ? 0 : src.depth_max() - 1;
     for (int L = hi; L >= lo; --L) {
         if (src.level_count[L] == 0) continue;
-        k_m2m<<<src.level_count[L], kPassThreads, sm_m2m, s>>>(v, cheb, src.level_first[L], src.qw, mode, own);
+        if (sm_m2m4 <= 48 * 1024)
+            k_m2m4<<<src.level_count[L], kM2mGroups * kPassThreads, sm_m2m4, s>>>(v, cheb, src.level_first[L], src.qw,
+                                                                                mode, own);
+        else
+            k_m2m<<<src.level_count[L], kPassThreads, sm_m2m, s>>>(v, cheb, src.level_first[L], src.qw, mode, own);
         CSFS_LAUNCH_CHECK();
     }
 }
