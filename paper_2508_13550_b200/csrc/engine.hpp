@@ -166,6 +166,10 @@ struct Items {
     DevBuf<long long> mpoff, mlist, unit_b;
     DevBuf<double> partial;
     DevBuf<int> oitem, opair, ocnt, otiles;  // a rank's own items / pairs (interact.cu compact_owned)
+    // ordering the items by cost (traverse.cu order_items_by_cost): sort scratch, permuted copies
+    DevBuf<int> skey, skb, svb, sout, shist, stiles, sgrand, keys2, anchor2;
+    DevBuf<int4> item2;
+    DevBuf<double> cost2;
     int n_mutual = 0;
     long long n_partial = 0;  // doubles
     unsigned long long skipped_pairs = 0;

@@ -16,6 +16,7 @@
 #include "scan.cuh"
 
 namespace csfs_b200 {
+namespace {  // internal linkage: every translation unit that sorts gets its own kernels
 
 constexpr int kRadixThreads = 256;
 constexpr int kRadixRows = 16;
@@ -134,4 +135,5 @@ inline const int* radix_sort_positions(long long n, int bits, int* keys, int* kb
     return vout;
 }
 
+}  // namespace
 }  // namespace csfs_b200

@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "engine.hpp"
+#include "radix.cuh"
 #include "scan.cuh"
 
 namespace csfs_b200 {
@@ -619,6 +620,60 @@ void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, in
     }
 }
 
+namespace {
+// Item sort key: the cost's double bit pattern (monotone for non-negative doubles) cut to
+// exponent + 8 mantissa bits, i.e. costs to within 0.4%: 13 bits, two radix passes.
+__global__ void k_cost_key(int n, const double* __restrict__ cost, int* key) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long b = (long long)(__double_as_longlong(cost[i]) >> 44) - (1023ll << 8);
+    key[i] = int(b < 0 ? 0 : (b > 8191 ? 8191 : b));
+}
+
+__global__ void k_permute_items(int n, const int* __restrict__ order, const int* __restrict__ keys,
+                                const int4* __restrict__ item, const int* __restrict__ anchor,
+                                const double* __restrict__ cost, int* keys2, int4* item2, int* anchor2,
+                                double* cost2) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int i = order[j];
+    keys2[j] = keys[i];
+    item2[j] = item[i];
+    anchor2[j] = anchor[i];
+    cost2[j] = cost[i];
+}
+}  // namespace
+
+// Items in ascending cost (stable: key order among equal costs).  k_interact hands them out
+// back to front, so the most expensive go first and the kernel's tail is made of the
+// cheapest (longest-processing-time-first); nothing else depends on the item order — every
+// item owns its outputs and sums them in a fixed order.
+void order_items_by_cost(Items& it, cudaStream_t s) {
+    const int n = it.n_items;
+    if (n <= 1) return;
+    for (DevBuf<int>* b : {&it.skey, &it.skb, &it.svb, &it.sout, &it.keys2, &it.anchor2}) b->grow(n);
+    it.item2.grow(n);
+    it.cost2.grow(n);
+    const int ntiles = ceil_div(n, kRadixTile);
+    it.shist.grow(size_t(kRadixBins) * ntiles);
+    it.stiles.grow(scan_tile_ints((long long)kRadixBins * ntiles, 1));
+    it.sgrand.grow(8);
+    k_cost_key<<<ceil_div(n, 256), 256, 0, s>>>(n, it.cost, it.skey);
+    CSFS_LAUNCH_CHECK();
+    const int* order = radix_sort_positions(n, 13, it.skey, it.skb, it.svb, it.sout, it.shist, it.stiles, it.sgrand, s);
+    k_permute_items<<<ceil_div(n, 256), 256, 0, s>>>(n, order, it.keys, it.item, it.anchor, it.cost, it.keys2,
+                                                     it.item2, it.anchor2, it.cost2);
+    CSFS_LAUNCH_CHECK();
+    std::swap(it.keys.p, it.keys2.p);
+    std::swap(it.keys.cap, it.keys2.cap);
+    std::swap(it.item.p, it.item2.p);
+    std::swap(it.item.cap, it.item2.cap);
+    std::swap(it.anchor.p, it.anchor2.p);
+    std::swap(it.anchor.cap, it.anchor2.cap);
+    std::swap(it.cost.p, it.cost2.p);
+    std::swap(it.cost.cap, it.cost2.cap);
+}
+
 void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, Items& it, Scratch& sc,
                  cudaStream_t s) {
     const TreeView T = tgt.view(), S = src.view();
@@ -675,6 +730,7 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, I
                                                          it.code, it.seg, it.item, it.anchor, it.cost,
                                                          T, S);
         CSFS_LAUNCH_CHECK();
+        order_items_by_cost(it, s);
     }
 }
 
