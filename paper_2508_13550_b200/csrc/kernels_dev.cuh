@@ -105,9 +105,11 @@ __device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
         const double r = kPi2Over6 - lu * ly - li2_bernoulli(-lu);
         return (u == 1.0) ? kPi2Over6 : r;
     }
-    // z = -log1p(-u) via the compensated form log(t) - ((t - 1) + u)/t, t = 1 - u
+    // z = -log1p(-u) via the compensated form log(t) - ((t - 1) + u)/t, t = 1 - u: the
+    // correction (t - 1) + u is t's rounding error (|.| <= 2^-53), so the bare MUFU
+    // reciprocal (2^-20) is enough — it moves z by < 2^-72
     const double t = 1.0 - u;
-    const double z = -(fast_log(t, tab) - ((t - 1.0) + u) * fast_rcp(t));
+    const double z = -(fast_log(t, tab) - ((t - 1.0) + u) * rcp_seed(t));
     return li2_bernoulli(z);
 }
 
