@@ -94,6 +94,7 @@ struct DeviceTree {
     DevBuf<double> xi0, xi1, eta0, eta1, cx, cy, cz, rad;
     DevBuf<unsigned char> split;
     DevBuf<unsigned long long> bnd;  // 4 per cluster: min xi, max xi, min eta, max eta (ordered)
+    DevBuf<double2> mid;             // per cluster: the split point (midpoint of the shrunk bounds)
     std::vector<int> level_first, level_count;
     std::vector<int> root_count;  // 6
     // proxies

@@ -59,11 +59,12 @@ struct ClusterPtrs {
     double *xi0, *xi1, *eta0, *eta1, *cx, *cy, *cz, *rad;
     unsigned char* split;
     unsigned long long* bnd;
+    double2* mid;
 };
 
 ClusterPtrs cluster_ptrs(DeviceTree& t) {
     return {t.face, t.depth, t.begin, t.end, t.parent, t.nchild, t.child, t.xi0, t.xi1,
-            t.eta0, t.eta1, t.cx,    t.cy,    t.cz,  t.rad,    t.split,  t.bnd};
+            t.eta0, t.eta1, t.cx,    t.cy,    t.cz,  t.rad,    t.split,  t.bnd, t.mid};
 }
 
 __global__ void k_roots(ClusterPtrs c, const int* grand) {
@@ -258,6 +259,7 @@ __device__ __forceinline__ bool geom_one(const ClusterPtrs& c, int id, bool shri
     const double ext = (ex < ey) ? ey : ex;  // std::max
     const bool sp = !(count <= n0 || c.depth[id] >= kMaxDepth) && !(ext < kMinExtent);
     c.split[id] = sp ? 1 : 0;
+    c.mid[id] = make_double2(xm, em);  // the split point quadrant_of derives (:98-99)
     return sp;
 }
 
@@ -801,12 +803,20 @@ __global__ void __launch_bounds__(kRunThreads)
     }
 #pragma unroll
     for (int j = 0; j < kRun; ++j) nd[j] = v[j] < 0 ? qchild[-v[j] - 1] : v[j];
+    int cur = -1;  // the thread's particles often share a cluster: its split flag and point once
+    bool csp = false;
+    double2 cm = make_double2(0.0, 0.0);
 #pragma unroll
     for (int j = 0; j < kRun; ++j) {
         const long long i = base + j * kRunThreads;
         int key = -1;
-        if (nd[j] >= L.first && nd[j] < L.first + L.cnt && c.split[nd[j]]) {
-            key = 4 * nd[j] + quadrant_of(c, nd[j], x[j], e[j]);
+        if (nd[j] != cur) {
+            cur = nd[j];
+            csp = cur >= L.first && cur < L.first + L.cnt && c.split[cur];
+            if (csp) cm = c.mid[cur];
+        }
+        if (csp) {
+            key = 4 * nd[j] + (x[j] >= cm.x ? 1 : 0) + (e[j] >= cm.y ? 2 : 0);  // quadrant_of
             lab[i] = -(key + 1);
         } else if (v[j] < 0) {
             lab[i] = nd[j];
@@ -1056,6 +1066,7 @@ void DeviceTree::reserve_clusters(int n_needed, cudaStream_t s) {
     rad.grow_keep(c, u, s);
     split.grow_keep(c, u, s);
     bnd.grow_keep(4 * c, 4 * u, s);
+    mid.grow_keep(c, u, s);
     cap = int(c);
 }
 
