@@ -1,20 +1,24 @@
 // GPU cluster-tree build: the B200 restatement of csfs::ClusterTree's constructor
 // (/root/reference/proj/src/cluster_tree.cpp:29-147).
 //
-// The reference builds the quadtree serially with a LIFO stack.  Every split
-// decision only depends on the node's own particles (shrunk bounds -> midpoint ->
-// quadrant -> stable 4-way partition), so the same tree is produced level by level:
-//   level 0 : face_project per particle (K1), stable bucketing by face (K2 = 6-way scan)
-//   level d : for every splitting node, quadrant keys, one global 4-counter scan, a
-//             single-CTA child allocator (children in parent order, empties pruned),
-//             and a scatter that keeps each node's range contiguous (K3)
-//   per level: shrunk bounds and centre by warp-accumulated integer atomics on
-//             order-preserving encodings (exact, so deterministic)   (K4); only xi, eta,
-//             perm and node move between levels
-//   at the end: positions/weights gathered once through perm, every radius in one pass
-//             (a warp per leaf over its ancestors)
+// The reference builds the quadtree serially with a LIFO stack.  Every split decision only
+// depends on the node's own particles — their COUNT and shrunk BOUNDS (midpoint ->
+// quadrant), both order independent — and the composition of its stable 4-way partitions
+// is one stable sort of the particles by leaf.  So the default build (build_tree):
+//   level 0 : face_project per particle, the face as its label, the six roots' counts and
+//             bounds (k_face_label, k_root_geom)
+//   level d : particles of splitting frontier clusters take the label "quadrant q of
+//             cluster p" while per-(cluster, quadrant) counts and bounds accumulate
+//             (k_label); the frontier's children are allocated on the device in parent and
+//             quadrant order (k_alloc_scan, k_alloc_fill); no host round trip inside a
+//             batch of levels
+//   at the end: one stable radix sort of the particles by their leaf's first tree-order
+//             slot (radix.cuh) -> perm; positions and face coordinates gathered once;
+//             every radius in one pass (a warp per leaf over its ancestors)
+// The level-synchronous build of rounds 1-2 (the particles partitioned level by level,
+// CSFS_B200_TREE=levels) is kept for A/B and as the bitwise cross-check of the default.
 // Internal cluster ids are level-major (BFS); reference_ids() maps them onto the
-// reference's LIFO numbering for export (K5).  Particle data stays SoA in HBM.
+// reference's LIFO numbering for export.  Particle data stays SoA in HBM.
 #include <algorithm>
 #include <climits>
 #include <cmath>
@@ -117,60 +121,7 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     return v;
 }
 
-// Segmented min/max over each new cluster's particles.  Particles of a cluster are
-// contiguous, so a warp usually sees one cluster: each thread walks kSegItems strided
-// particles, the warp reduces each step and keeps a running result per cluster, and only
-// flushes it (integer atomics on order-preserving encodings: exact, order independent)
-// when the cluster changes.  Mixed warps (cluster boundaries) fall back to per-lane
-// atomics.  V values per particle; op[v] = 0 min, 1 max.
-constexpr int kSegItems = 8;
-
-template <int V>
-struct SegAcc {
-    int cur = -1;
-    unsigned long long acc[V];
-};
-
-template <int V>
-__device__ __forceinline__ void seg_flush(SegAcc<V>& s, unsigned long long* dst, const int (&op)[V]) {
-    if (s.cur >= 0 && (threadIdx.x & 31) == 0)
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            if (op[v]) atomicMax(&dst[(long long)s.cur * V + v], s.acc[v]);
-            else atomicMin(&dst[(long long)s.cur * V + v], s.acc[v]);
-        }
-    s.cur = -1;
-}
-
-template <int V>
-__device__ __forceinline__ void seg_step(SegAcc<V>& s, int nd, const unsigned long long (&val)[V],
-                                         unsigned long long* dst, const int (&op)[V]) {
-    const int nd0 = __shfl_sync(0xffffffffu, nd, 0);
-    if (__all_sync(0xffffffffu, nd == nd0)) {
-        if (nd0 < 0) return;
-        unsigned long long r[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) r[v] = op[v] ? warp_max_u64(val[v]) : warp_min_u64(val[v]);
-        if (nd0 != s.cur) {
-            seg_flush<V>(s, dst, op);
-            s.cur = nd0;
-#pragma unroll
-            for (int v = 0; v < V; ++v) s.acc[v] = r[v];
-        } else {
-#pragma unroll
-            for (int v = 0; v < V; ++v)
-                s.acc[v] = op[v] ? (r[v] > s.acc[v] ? r[v] : s.acc[v]) : (r[v] < s.acc[v] ? r[v] : s.acc[v]);
-        }
-    } else {
-        seg_flush<V>(s, dst, op);
-        if (nd >= 0)
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                if (op[v]) atomicMax(&dst[(long long)nd * V + v], val[v]);
-                else atomicMin(&dst[(long long)nd * V + v], val[v]);
-            }
-    }
-}
+constexpr int kSegItems = 8;  // consecutive particles per thread in k_bounds
 
 // Shrunk bounds: min/max of xi, eta over each new cluster's particles (:53-61).  Each thread
 // first reduces kSegItems CONSECUTIVE particles in registers (a cluster change inside the
