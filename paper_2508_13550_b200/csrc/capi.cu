@@ -359,28 +359,42 @@ void part_plan(csfs_b200_ctx* c, const double* txyz, size_t nt, const double* sx
     CSFS_CK(cudaStreamWaitEvent(ls, c->ev[10], 0));
     dual_traversal(T, S, f.mac, n0, c->lists, c->sc, ls);
     mark("traversal");
-    build_items(T, S, c->lists, c->items, c->sc, ls);
-    mark("items");
-    prepare_mutual(c, ls, false);  // unit scope: the same pairs for every rank count
-    mark("mutual");
+    // target units' costs: the pair evaluations of their list entries, summed on the device
+    // in exact integer arithmetic (every rank must derive the same split)
+    const int nu = int(c->unit_b[0].size());
+    c->ubeg.grow(std::max(nu, 1));
+    c->ucost.grow(std::max(nu, 1));
+    CSFS_CK(cudaMemcpyAsync(c->ubeg.p, c->unit_b[0].data(), nu * sizeof(long long), cudaMemcpyHostToDevice, ls));
+    CSFS_CK(cudaMemsetAsync(c->ucost.p, 0, std::max(nu, 1) * sizeof(unsigned long long), ls));
+    list_unit_costs(T, S, c->lists, c->ubeg.p, nu, c->ucost.p, ls);
     {
-        // target units' costs: the pair evaluations of their items, summed on the device in
-        // exact integer arithmetic (every rank must derive the same split)
-        const int ni = c->items.n_items, nu = int(c->unit_b[0].size());
-        c->ubeg.grow(std::max(nu, 1));
-        c->ucost.grow(std::max(nu, 1));
-        CSFS_CK(cudaMemcpyAsync(c->ubeg.p, c->unit_b[0].data(), nu * sizeof(long long), cudaMemcpyHostToDevice, ls));
-        CSFS_CK(cudaMemsetAsync(c->ucost.p, 0, std::max(nu, 1) * sizeof(unsigned long long), ls));
-        unit_costs(c->items, ni, c->ubeg.p, nu, c->ucost.p, ls);
         std::vector<unsigned long long> uc(std::max(nu, 1));
         CSFS_CK(cudaMemcpyAsync(uc.data(), c->ucost.p, std::max(nu, 1) * sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, ls));
         CSFS_CK(cudaStreamSynchronize(ls));
         for (int u = 0; u < nu; ++u) c->unit_cost[0][u] = double(uc[u]);
     }
+    mark("costs");
+    if (early_upward) {  // the group rank program: the target split now, and only our items
+        const int R = c->nranks;
+        const auto trun = split_contiguous(c->unit_cost[0], R);
+        c->t_range.assign(2 * R, 0);
+        for (int r = 0; r < R; ++r)
+            if (trun[r].second > trun[r].first) {
+                c->t_range[2 * r] = c->unit_b[0][trun[r].first];
+                c->t_range[2 * r + 1] = c->unit_e[0][trun[r].second - 1];
+            }
+        const long long ob = c->t_range[2 * c->rank], oe = c->t_range[2 * c->rank + 1];
+        const long long n = (long long)T.n;
+        build_items(T, S, c->lists, c->items, c->sc, ls, oe > ob ? ob : n, oe > ob ? oe : n);
+    } else {
+        build_items(T, S, c->lists, c->items, c->sc, ls);
+    }
+    mark("items");
+    prepare_mutual(c, ls, false);  // unit scope: the same pairs for every rank count
+    mark("mutual");
     CSFS_CK(cudaEventRecord(c->ev[10], ls));  // the lists are ready for work on s
     CSFS_CK(cudaStreamWaitEvent(s, c->ev[10], 0));
-    mark("costs");
     if (trace) {
         for (size_t i = 1; i < marks.size(); ++i)
             fprintf(stderr, "plan %s %.3f ms\n", marks[i].first, marks[i].second - marks[i - 1].second);

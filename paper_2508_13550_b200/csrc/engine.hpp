@@ -222,17 +222,19 @@ void downward_pass(DeviceTree& tgt, const Cheb& cheb, int dim, const double* phi
 // traverse.cu
 void dual_traversal(const DeviceTree& tgt, const DeviceTree& src, double mac, int n0, Lists& lists,
                     Scratch& sc, cudaStream_t s);
+// own_b >= 0: only items of targets whose first particle lies in [own_b, own_e), plus the
+// depth-0 targets every rank evaluates (the group plan); own_b < 0: every target.
 void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& lists, Items& items,
-                 Scratch& sc, cudaStream_t s);
+                 Scratch& sc, cudaStream_t s, long long own_b = -1, long long own_e = -1);
 // Symmetric PP marking (shared tree only); unit_begins = sorted first particles of the
 // partition units (depth-1 subtrees + unsplit roots).
 void build_mutual(const DeviceTree& tgt, Items& items, const std::vector<long long>& unit_begins, Scratch& sc,
                   cudaStream_t s);
 // Partition units of a tree: (begin, end) particle ranges in tree order.
 void partition_units(const DeviceTree& t, std::vector<long long>& b, std::vector<long long>& e, cudaStream_t s);
-// Pair evaluations of the items anchored in each unit (ubeg: the units' first particles).
-void unit_costs(const Items& it, int n_items, const long long* ubeg, int nu, unsigned long long* ucost,
-                cudaStream_t s);
+// Pair evaluations of the list entries of each target unit (ubeg: the units' first particles).
+void list_unit_costs(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, const long long* ubeg, int nu,
+                     unsigned long long* ucost, cudaStream_t s);
 
 // interact.cu
 void interact(const KernelSpec& k, const DeviceTree& tgt, const DeviceTree& src, Items& items,

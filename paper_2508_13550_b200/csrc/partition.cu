@@ -188,11 +188,6 @@ void exchange_order(csfs_b200_ctx* c, const DeviceTree& S, cudaStream_t s) {
 
 namespace {
 
-std::pair<long long, long long> owned_range(const std::vector<long long>& b, const std::vector<long long>& e,
-                                            std::pair<int, int> run) {
-    if (run.second <= run.first) return {0, 0};
-    return {b[run.first], e[run.second - 1]};
-}
 
 // Phase A: plan, split, owned upward pass, own segment packed into xq.
 void phase_plan(Ctx* c, const Inputs& in, const KernelSpec& ks, const FmmConfig& f, cudaStream_t s) {
@@ -201,14 +196,7 @@ void phase_plan(Ctx* c, const Inputs& in, const KernelSpec& ks, const FmmConfig&
     // the owned upward pass starts inside the plan, under the traversal (part_plan early_upward)
     capi::part_plan(c, in.txyz, in.nt, in.sxyz, in.sw, in.ns, ks, f, s, true);
     CSFS_CK(cudaEventRecord(ev[1], s));
-    const int R = c->nranks;
-    const auto trun = split_contiguous(c->unit_cost[0], R);
-    c->t_range.assign(2 * R, 0);
-    for (int r = 0; r < R; ++r) {
-        const auto t = owned_range(c->unit_b[0], c->unit_e[0], trun[r]);
-        c->t_range[2 * r] = t.first;
-        c->t_range[2 * r + 1] = t.second;
-    }
+    // c->t_range (the target split) is set by part_plan, which built only our items
     DeviceTree& S = c->shared ? c->ttree : c->stree;
     CSFS_CK(cudaStreamWaitEvent(s, ev[11], 0));  // the owned upward pass (aux)
     // c->xidx / c->xq_off: the exchange order, set by part_plan (exchange_order)

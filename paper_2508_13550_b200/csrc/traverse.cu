@@ -90,13 +90,20 @@ __device__ __forceinline__ bool can_fuse(const TreeView& T, const TreeView& S, i
     return R - rt - rs > kFuseGap;
 }
 
+// A target cluster is ours when the range is everything, it is at depth 0 (every rank
+// evaluates those), or its first particle lies in [own_b, own_e).
+__device__ __forceinline__ bool owned_target(const TreeView& T, int t, long long own_b, long long own_e) {
+    return own_b < 0 || T.depth[t] == 0 || (T.begin[t] >= own_b && T.begin[t] < own_e);
+}
+
 __global__ void k_count(const int2* __restrict__ l, long long n, int key_off, int* cnt,
-                        const TreeView T, const TreeView S, int type, unsigned long long* pairs) {
+                        const TreeView T, const TreeView S, int type, unsigned long long* pairs, long long own_b,
+                        long long own_e) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long pe = 0;
     if (i < n) {
         const int2 ts = l[i];
-        atomicAdd(&cnt[key_off + ts.x], 1);
+        if (owned_target(T, ts.x, own_b, own_e)) atomicAdd(&cnt[key_off + ts.x], 1);
         const long long nt = (type <= 1) ? (T.end[ts.x] - T.begin[ts.x]) : T.npp;
         const long long ns = (type == 0 || type == 2) ? (S.end[ts.y] - S.begin[ts.y]) : S.npp;
         pe = (unsigned long long)(nt * ns);
@@ -107,10 +114,12 @@ __global__ void k_count(const int2* __restrict__ l, long long n, int key_off, in
 }
 
 __global__ void k_fill(const int2* __restrict__ l, long long n, int key_off, int type,
-                       const int* __restrict__ off, int* cur, long long* code) {
+                       const int* __restrict__ off, int* cur, long long* code, const TreeView T, long long own_b,
+                       long long own_e) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int2 ts = l[i];
+    if (!owned_target(T, ts.x, own_b, own_e)) return;
     const int key = key_off + ts.x;
     const int slot = off[key] + atomicAdd(&cur[key], 1);
     code[slot] = ((long long)type << 32) | (unsigned)ts.y;
@@ -359,32 +368,46 @@ __global__ void __launch_bounds__(256) k_traverse_step(const TreeView T, const T
 }  // namespace
 
 namespace {
-// Each item's pair evaluations into its target unit (the last unit beginning at or before
-// its anchor); u64 atomics: exact, so the sum is order independent.
-__global__ void k_unit_costs(int n_items, const int* __restrict__ anchor, const double* __restrict__ cost,
-                             const long long* __restrict__ ubeg, int nu, unsigned long long* ucost) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// Each list entry's pair evaluations into its target's unit (depth-0 targets excluded:
+// every rank evaluates them); lanes that share a unit combine first (per-entry costs are
+// below 2^16, so 32 of them fit the 32-bit reduction), then one u64 atomic: exact.
+__global__ void k_list_unit_costs(const int2* __restrict__ l, long long n, int type, const TreeView T,
+                                  const TreeView S, const long long* __restrict__ ubeg, int nu,
+                                  unsigned long long* ucost) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     int u = -1;
-    unsigned long long v = 0;
-    if (i < n_items && anchor[i] >= 0) {
-        int lo = 0, hi = nu;  // first unit with ubeg > anchor
-        while (lo < hi) {
-            const int m = (lo + hi) >> 1;
-            if (ubeg[m] <= anchor[i]) lo = m + 1;
-            else hi = m;
+    unsigned v = 0;
+    if (i < n) {
+        const int2 ts = l[i];
+        if (T.depth[ts.x] > 0) {
+            const long long a = T.begin[ts.x];
+            int lo = 0, hi = nu;  // first unit beginning after a
+            while (lo < hi) {
+                const int m = (lo + hi) >> 1;
+                if (ubeg[m] <= a) lo = m + 1;
+                else hi = m;
+            }
+            u = lo - 1;
+            const long long nt = (type <= 1) ? (T.end[ts.x] - T.begin[ts.x]) : T.npp;
+            const long long ns = (type == 0 || type == 2) ? (S.end[ts.y] - S.begin[ts.y]) : S.npp;
+            v = unsigned(nt * ns);
         }
-        u = lo - 1;
-        v = (unsigned long long)cost[i];
     }
-    if (u >= 0) atomicAdd(&ucost[u], v);
+    const unsigned peers = __match_any_sync(0xffffffffu, u);
+    if (u < 0) return;
+    const unsigned long long sum = __reduce_add_sync(peers, v);
+    if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&ucost[u], sum);
 }
 }  // namespace
 
-void unit_costs(const Items& it, int n_items, const long long* ubeg, int nu, unsigned long long* ucost,
-                cudaStream_t s) {
-    if (n_items <= 0 || nu <= 0) return;
-    k_unit_costs<<<ceil_div(n_items, 256), 256, 0, s>>>(n_items, it.anchor, it.cost, ubeg, nu, ucost);
-    CSFS_LAUNCH_CHECK();
+void list_unit_costs(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, const long long* ubeg, int nu,
+                     unsigned long long* ucost, cudaStream_t s) {
+    const TreeView T = tgt.view(), S = src.view();
+    for (int k = 0; k < 4; ++k) {
+        if (L.n[k] == 0 || nu <= 0) continue;
+        k_list_unit_costs<<<ceil_div(L.n[k], 256), 256, 0, s>>>(L.l[k], L.n[k], k, T, S, ubeg, nu, ucost);
+        CSFS_LAUNCH_CHECK();
+    }
 }
 
 void partition_units(const DeviceTree& t, std::vector<long long>& ub, std::vector<long long>& ue, cudaStream_t s) {
@@ -675,7 +698,7 @@ void order_items_by_cost(Items& it, cudaStream_t s) {
 }
 
 void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, Items& it, Scratch& sc,
-                 cudaStream_t s) {
+                 cudaStream_t s, long long own_b, long long own_e) {
     const TreeView T = tgt.view(), S = src.view();
     const int ncl_t = tgt.ncl;
     const int nkeys = 2 * ncl_t;
@@ -690,7 +713,7 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, I
     for (int k = 0; k < 4; ++k) {
         if (L.n[k] == 0) continue;
         k_count<<<ceil_div(L.n[k], kThreads), kThreads, 0, s>>>(L.l[k], L.n[k], k <= 1 ? 0 : ncl_t,
-                                                                 it.cnt, T, S, k, it.pairs);
+                                                                 it.cnt, T, S, k, it.pairs, own_b, own_e);
         CSFS_LAUNCH_CHECK();
     }
     sc.tiles.grow(scan_tile_ints(nkeys, 2));
@@ -722,7 +745,7 @@ void build_items(const DeviceTree& tgt, const DeviceTree& src, const Lists& L, I
     for (int k = 0; k < 4; ++k) {
         if (L.n[k] == 0) continue;
         k_fill<<<ceil_div(L.n[k], kThreads), kThreads, 0, s>>>(L.l[k], L.n[k], k <= 1 ? 0 : ncl_t, k,
-                                                                it.off, it.cur, it.code);
+                                                                it.off, it.cur, it.code, T, own_b, own_e);
         CSFS_LAUNCH_CHECK();
     }
     if (it.n_items) {
