@@ -507,7 +507,11 @@ int csfs_b200_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const doubl
         }
         c->h_w.grow(ns);
         // the weights are first needed after the tree levels: copy them on the aux stream
-        // while the positions' tree is built
+        // while the positions' tree is built — after the positions, which the build needs
+        // first (two concurrent host-to-device copies share the PCIe link and would delay
+        // the positions by the weights' transfer time)
+        CSFS_CK(cudaEventRecord(c->ev[10], s));
+        CSFS_CK(cudaStreamWaitEvent(c->aux, c->ev[10], 0));
         CSFS_CK(cudaMemcpyAsync(c->h_w.p, sw, ns * sizeof(double), cudaMemcpyHostToDevice, c->aux));
         CSFS_CK(cudaEventRecord(c->w_copied, c->aux));
         const size_t nout = nt * size_t(ks.out_dim());
