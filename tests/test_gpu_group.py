@@ -73,6 +73,24 @@ def test_emulated_groups_bitwise(unit_engine, name, level, kname):
         g.close()
 
 
+def test_more_ranks_than_units_bitwise(unit_engine):
+    """More ranks than partition units (24 depth-1 subtrees): the extra ranks own no
+    targets and no sources — they build only the depth-0 items, send empty segments and
+    still receive the full result — and the result is the same bits."""
+    wl, k, cfg = _inputs("c2", 5, None)
+    p = ParticleSet(wl.xyz, wl.weights)
+    want = unit_engine.csfmm_sum(p, p, k, cfg).values.copy()
+    g = Engine.emulated(0, 30)
+    st = SumStats()
+    np.testing.assert_array_equal(g.csfmm_sum(p, p, k, cfg, st).values, want)
+    info = g.group_info()
+    assert sum(1 for r in info["target_ranges"] if r[1] <= r[0]) >= 6
+    u = SumStats()
+    unit_engine.csfmm_sum(p, p, k, cfg, u)
+    assert st.evals_executed == u.evals_executed
+    g.close()
+
+
 def test_group_executed_evaluations_add_up(unit_engine):
     """The executed evaluations the ranks report sum to the one-rank count (the roofline of
     an N-GPU bench line is this sum / N peaks); grid inputs have no depth-0 target items."""
