@@ -224,16 +224,17 @@ struct OpSalT {
     // y ~ 1/sqrt(hom) = 2/gamma.
     __device__ __forceinline__ static double tgt(double x) { return 0.5 * x; }
     // 2/gamma and log(s (1 + s)), s = gamma/2 = sqrt(hom): cubic correction of the seed,
-    // e = 1 - hom y^2, c = e/2 + 3e^2/8, 2/gamma = y (1 + c), s = hom y (1 + c).  Returns
-    // 2/gamma + 2k log(...) (scale() carries the 1/2), or the log alone.
+    // e = 1 - hom y^2, c = e/2 + 3e^2/8, 2/gamma = 1/s = y (1 + c); then s (1 + s) = s + s^2
+    // = hom (1/s) + hom in ONE fma (s^2 = hom: no separate s), within ~3 ulp like the
+    // s-then-fma(s, s, s) form it replaces.  Returns 2/gamma + 2k log(...) (scale() carries
+    // the 1/2), or the log alone.
     __device__ __forceinline__ double kernel(double hom, const LogTable& tab) const {
         const double y = rsqrt_seed(hom);
         const double h = hom * y;
         const double e = fma(-h, y, 1.0);
         const double c = e * fma(e, 0.375, 0.5);
-        const double r2 = fma(y, c, y);  // 2/gamma
-        const double s = fma(h, c, h);   // gamma/2, off r2's chain
-        const double L = fast_log(fma(s, s, s), tab);
+        const double r2 = fma(y, c, y);  // 2/gamma = 1/s
+        const double L = fast_log(fma(hom, r2, hom), tab);
         return kLogOnly ? L : fma(k, L, r2);
     }
     template <bool G = true, bool F = false>
