@@ -12,9 +12,10 @@
 //  * the prefactor (-1/4pi, 1/4pi, 3 rho/4pi) is applied once per target (`scale`);
 //  * log / rsqrt / rcp come from fastmath.cuh (6 / 5 / 3 FP64 instructions instead of
 //    libdevice's ~28 / 8+8 / 8), each within a few ulp;
-//  * SAL: targets enter halved, so 0.5 - t'.s = omc/2 exactly; 2/gamma = rsqrt(omc/2),
-//    s = gamma/2 = (omc/2) rsqrt(omc/2), log(s (1 + s)) = log(fma(s, s, s)) — the
-//    reference's formula, without sqrt, divide or a seed rescale.
+//  * SAL: targets enter halved, so hom = 0.5 - t'.s = omc/2 exactly; 2/gamma = 1/s =
+//    rsqrt(hom) with s = gamma/2, and log(s (1 + s)) = log(s + s^2) = log(fma(hom, 1/s,
+//    hom)) since s^2 = hom — the reference's formula, without sqrt, divide, a seed rescale
+//    or s itself.
 #pragma once
 
 #include "common.cuh"
