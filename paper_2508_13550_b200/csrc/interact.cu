@@ -79,6 +79,17 @@ template <class Op>
 struct MinBlocksOf<Op, std::void_t<decltype(Op::kMinBlocks)>> {
     static constexpr int value = Op::kMinBlocks;
 };
+// Ops whose far-field sum factors through the source positions (Biot-Savart:
+// sum_s a_s (t x s) = t x sum_s a_s s): Op::kFarFactored, eval_far, far_finish
+template <class Op, class = void>
+struct FarOf {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct FarOf<Op, std::void_t<decltype(Op::kFarFactored)>> {
+    static constexpr bool value = Op::kFarFactored;
+};
+
 #ifndef CSFS_MTPT
 #define CSFS_MTPT 2
 #endif
@@ -159,6 +170,11 @@ __global__ void __launch_bounds__(kIB, MinBlocksOf<Op>::value) k_interact(Intera
         for (int t0 = 0; t0 < tlen; t0 += gs * kTPT) {
             const bool grp = g < G;
             double tx[kTPT], ty[kTPT], tz[kTPT], acc[kTPT][D];
+            constexpr bool kFar = FarOf<Op>::value;
+            double far[kFar ? kTPT : 1][3];  // far-field source moments (FarOf ops)
+            if constexpr (kFar)
+#pragma unroll
+                for (int k = 0; k < kTPT; ++k) far[k][0] = far[k][1] = far[k][2] = 0.0;
             bool act[kTPT];
 #pragma unroll
             for (int k = 0; k < kTPT; ++k) {
@@ -196,8 +212,12 @@ __global__ void __launch_bounds__(kIB, MinBlocksOf<Op>::value) k_interact(Intera
                     for (int j = jb; j < je; ++j) {
                         const double2 a = sxy[j], b = szw[j];
 #pragma unroll
-                        for (int k = 0; k < kTPT; ++k)
-                            op.template eval<false, true>(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, acc[k], tab);
+                        for (int k = 0; k < kTPT; ++k) {
+                            if constexpr (kFar)
+                                op.eval_far(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, far[k], tab);
+                            else
+                                op.template eval<false, true>(tx[k], ty[k], tz[k], a.x, a.y, b.x, b.y, acc[k], tab);
+                        }
                     }
                 } else {
 #pragma unroll kU
@@ -262,6 +282,9 @@ __global__ void __launch_bounds__(kIB, MinBlocksOf<Op>::value) k_interact(Intera
                 guarded = fguard;
                 fused = ffused;
             }
+            if constexpr (kFar)
+#pragma unroll
+                for (int k = 0; k < kTPT; ++k) op.far_finish(tx[k], ty[k], tz[k], far[k], acc[k]);
             if (G > 1) {
 #pragma unroll
                 for (int k = 0; k < kTPT; ++k)

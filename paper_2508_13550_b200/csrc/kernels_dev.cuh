@@ -145,7 +145,28 @@ struct OpBiharmonic {
 
 struct OpBiotSavart {
     static constexpr bool kFusable = true;  // has a fused 1 - x.y form (one_minus_dot<true>)
+    // far entries (the fused ones): sum_s a_s (t x s) = t x (sum_s a_s s), a_s = w_s/(1 - t.s):
+    // eval_far accumulates the moment sum_s a_s s (3 FMAs per pair instead of a cross product
+    // and 3 FMAs) and far_finish adds t x moment once per target.  Far pairs are > kFuseGap
+    // apart, so the moment has no near-coincidence cancellation to preserve.
+#ifndef CSFS_BS_FAR_MOMENT
+#define CSFS_BS_FAR_MOMENT 1
+#endif
+    static constexpr bool kFarFactored = CSFS_BS_FAR_MOMENT;
     static constexpr int dim = 3;
+    __device__ __forceinline__ void eval_far(double tx, double ty, double tz, double sx, double sy, double sz,
+                                             double sw, double* m, const LogTable&) const {
+        const double omc = one_minus_dot<true>(1.0, tx, ty, tz, sx, sy, sz);
+        const double a = sw * fast_rcp(omc);
+        m[0] = fma(a, sx, m[0]);
+        m[1] = fma(a, sy, m[1]);
+        m[2] = fma(a, sz, m[2]);
+    }
+    __device__ __forceinline__ static void far_finish(double tx, double ty, double tz, const double* m, double* acc) {
+        acc[0] += fma(ty, m[2], -(tz * m[1]));
+        acc[1] += fma(tz, m[0], -(tx * m[2]));
+        acc[2] += fma(tx, m[1], -(ty * m[0]));
+    }
     static constexpr double kSym = -1.0;  // cross(s, t) = -cross(t, s), 1 - s.t = 1 - t.s
     __device__ __forceinline__ static double tgt(double x) { return x; }
     __device__ __forceinline__ double scale() const { return -kInv4Pi; }
