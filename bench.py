@@ -424,6 +424,9 @@ def run_ours(args, rt=None, engine_factory=None, clock_factory=None, fp64_peak=N
             "executed_flop_per_pair": fpp,
             "executed_pair_evals_per_launch": exec_evals,
             "list_pair_evals_per_launch": list_evals,
+            # the evaluation throughput itself (flop-count independent: a functor that needs
+            # fewer FP64 operations per pair lowers `frac` while raising this)
+            "executed_evals_per_s_per_gpu": exec_evals / t_int / world,
             "fp64_pipe_active_pct_ncu": ncu.get("fp64_pipe_active_pct"),
             "frac_of_nominal_37.2": achieved / NOMINAL_FP64_TFLOPS if achieved else None,
             "step_frac": (exec_evals * fpp / (ms_per_step * 1e-3) / 1e12 / world / peak_mean) if fpp else None,
