@@ -146,9 +146,9 @@ __global__ void __launch_bounds__(kIB, MinBlocksOf<Op>::value) k_interact(Intera
 #ifndef CSFS_ITEM_ORDER_REVERSED
 #define CSFS_ITEM_ORDER_REVERSED 1
 #endif
-        // the queue hands out the items back to front: cluster items (CP/CC, the largest,
-        // up to ~1.3M evaluations each at C5) first, the uniform leaf items last, so the
-        // kernel's tail is made of short items (longest-first scheduling)
+        // the queue hands out the items back to front: build_items sorted them by cost
+        // (traverse.cu order_items_by_cost), so the most expensive go first and the
+        // kernel's tail is made of the cheapest (longest-processing-time first)
         const int iq = CSFS_ITEM_ORDER_REVERSED ? n_items - 1 - q : q;
         const int it = P.idx ? P.idx[iq] : iq;
         if (P.anchor) {
