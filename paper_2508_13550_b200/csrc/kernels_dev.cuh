@@ -92,10 +92,15 @@ __device__ __forceinline__ double li2_bernoulli(double z) {
     p = fma(p, w, 0x1.3d079fb6ef3e3p-18);
     p = fma(p, w, -0x1.23456789abcdfp-12);
     p = fma(p, w, 0x1.c71c71c71c71cp-6);  // B2/3! = 1/36
-    // z - z^2/4 + z^3 p(z^2)
-    return fma(z * w, p, fma(-0.25 * z, z, z));
+    // z - z^2/4 + z^3 p(z^2) = z + z^2 (z p - 1/4): two FMAs after the Horner chain; the
+    // rounding of (z p - 1/4) moves the result by <= z^2/4 2^-53 <= 1.3e-17 absolutely
+    return fma(w, fma(z, p, -0.25), z);
 }
 
+// C = false (the provably far entries, whose u already carries the fused form's few-ulp
+// absolute difference): z = -log(t) without the compensation term, which only corrects t's
+// own rounding (<= 2^-53 absolutely) — 4 FP64 instructions and a MUFU fewer.
+template <bool C = true>
 __device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
     constexpr double kPi2Over6 = kPi * kPi / 6.0;
     if (u > 0.5) {
@@ -109,32 +114,39 @@ __device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
     // correction (t - 1) + u is t's rounding error (|.| <= 2^-53), so the bare MUFU
     // reciprocal (2^-20) is enough — it moves z by < 2^-72
     const double t = 1.0 - u;
-    const double z = -(fast_log(t, tab) - ((t - 1.0) + u) * rcp_seed(t));
+    const double z = C ? -(fast_log(t, tab) - ((t - 1.0) + u) * rcp_seed(t)) : -fast_log(t, tab);
     return li2_bernoulli(z);
 }
 
+// BiharmonicOp: dilog(u) / 4pi, u = min(1, (1 + x.y)/2).  Targets enter halved (exact), so
+// the reference's 0.5 (1 + x.y) is 0.5 + t'.s bit for bit (scaling by 2 commutes with the
+// roundings): unfused in the reference's order, one DMUL fewer.  On the provably far entries
+// (F) u is three FMAs; it then differs from the reference's rounding by a few ulp of 1,
+// which moves the kernel by <= |dilog'(u)| 4e-16 = |ln(1 - u)/u| 4e-16 <= 5e-15 absolutely
+// (1 - u >= 5e-6 there) — u = (1 + x.y)/2 has no near-coincidence cancellation to
+// preserve.  The symmetric kernel keeps K(t, s) = K(s, t) bit for bit (exact products commute).
 struct OpBiharmonic {
     static constexpr int kMinBlocks = 3;
-    static constexpr bool kFusable = false;  // has a fused 1 - x.y form (one_minus_dot<true>)
+    static constexpr bool kFusable = true;  // has a fused form (u from three FMAs)
     static constexpr int dim = 1;
     static constexpr int kUnroll = 4;
     static constexpr double kSym = 1.0;
-    __device__ __forceinline__ static double tgt(double x) { return x; }
+    __device__ __forceinline__ static double tgt(double x) { return 0.5 * x; }
     __device__ __forceinline__ double scale() const { return kInv4Pi; }
+    template <bool F>
+    __device__ __forceinline__ static double u_of(double tx, double ty, double tz, double sx, double sy, double sz) {
+        const double u0 = F ? fma(tz, sz, fma(ty, sy, fma(tx, sx, 0.5))) : __dadd_rn(0.5, dot_ref(tx, ty, tz, sx, sy, sz));
+        return (u0 < 1.0) ? u0 : 1.0;  // std::min(1.0, u0)
+    }
     template <bool G = true, bool F = false>  // regular at coincidence: no guard either way
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
-        const double d = dot_ref(tx, ty, tz, sx, sy, sz);
-        const double u0 = __dmul_rn(0.5, __dadd_rn(1.0, d));
-        K[0] = dilog_dev((u0 < 1.0) ? u0 : 1.0, tab);
+        K[0] = dilog_dev<!F>(u_of<F>(tx, ty, tz, sx, sy, sz), tab);
     }
-    template <bool G = true, bool F = false>  // the dot stays unfused (u = (1 + x.y)/2 is not cancellation-prone)
+    template <bool G = true, bool F = false>
     __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
                                          double* acc, const LogTable& tab) const {
-        const double d = dot_ref(tx, ty, tz, sx, sy, sz);
-        const double u0 = __dmul_rn(0.5, __dadd_rn(1.0, d));
-        const double u = (u0 < 1.0) ? u0 : 1.0;  // std::min(1.0, u0)
-        acc[0] = fma(sw, dilog_dev(u, tab), acc[0]);
+        acc[0] = fma(sw, dilog_dev<!F>(u_of<F>(tx, ty, tz, sx, sy, sz), tab), acc[0]);
     }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,
