@@ -464,7 +464,7 @@ int csfs_b200_create_rank(csfs_b200_ctx** out, int device, int nranks, int rank,
     }
     ncclUniqueId u;
     std::memcpy(u.internal, id, CSFS_B200_NCCL_ID_BYTES);
-    CSFS_CK(cudaSetDevice(device));
+    if (cudaSetDevice(device) != cudaSuccess) return CSFS_B200_CUDA_ERROR;  // no exception across the C boundary
     if (ncclCommInitRank(&c->comm, nranks, u, rank) != ncclSuccess) return CSFS_B200_NCCL_ERROR;
     c->mode = Ctx::Mode::Rank;
     c->nranks = nranks;
