@@ -107,16 +107,17 @@ __global__ void __launch_bounds__(kRadixThreads)
 // holding the sorted positions (vb or out).  keys: the keys (clobbered); kb, vb, out:
 // scratch of n ints each; the passes alternate (keys, out) <-> (kb, vb).  hist: scratch of
 // 256 * ceil(n / 4096) ints; tiles/grand: scan scratch for 256 * ceil(n / 4096) counters.
+// low: bits [0, low) are equal in every key and are skipped.
 inline const int* radix_sort_positions(long long n, int bits, int* keys, int* kb, int* vb, int* out, int* hist,
-                                       int* tiles, int* grand, cudaStream_t s) {
+                                       int* tiles, int* grand, cudaStream_t s, int low = 0) {
     if (n <= 0) return out;
     const int ntiles = ceil_div(n, kRadixTile);
-    const int passes = std::max(1, (bits + 7) / 8);
+    const int passes = std::max(1, (bits - low + 7) / 8);
     const int* kin = keys;
     const int* vin = nullptr;
     int* vout = out;
     for (int p = 0; p < passes; ++p) {
-        const int shift = 8 * p;
+        const int shift = low + 8 * p;
         const bool last = p == passes - 1;
         int* kout = last ? nullptr : ((p & 1) ? keys : kb);
         vout = (p & 1) ? out : vb;

@@ -640,19 +640,53 @@ __device__ __forceinline__ void tile_accumulate(const TileStage& st, int* cnt, u
         }
         return;
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, r.key);
-    if (r.key < 0) return;
+    // The lanes hold consecutive runs of the tile, so the runs of one slot sit in ADJACENT
+    // lanes: a segmented reduction over the runs of equal-key adjacent lanes, five
+    // full-mask shuffle steps whatever the number of slots in the warp.  (match_any +
+    // redux.sync over each slot's lanes compiles to a loop over the distinct masks: at the
+    // deep levels of a grid, 16 slots per warp, that loop was 36% of the kernel's
+    // instructions and half of its stall samples — ncu, round 2.)  Equal keys in
+    // non-adjacent lanes (incoherent inputs) simply flush separately: the atomics combine
+    // them, exact and order independent either way.
+    constexpr unsigned kFull = 0xffffffffu;
+    const int kprev = __shfl_up_sync(kFull, r.key, 1);
+    const bool head = lane == 0 || kprev != r.key;
+    const unsigned heads = __ballot_sync(kFull, head);
     RunAcc t = r;
-    t.cnt = int(__reduce_add_sync(peers, unsigned(r.cnt)));
-    t.lo_x = redux_min_u64(peers, r.lo_x);
-    t.hi_x = redux_max_u64(peers, r.hi_x);
-    t.lo_e = redux_min_u64(peers, r.lo_e);
-    t.hi_e = redux_max_u64(peers, r.hi_e);
-    if ((peers & ((1u << lane) - 1u)) == 0) run_flush(t, cnt, bnd);
+    if (r.key < 0) {
+        t.cnt = 0;
+        t.lo_x = t.lo_e = ~0ull;
+        t.hi_x = t.hi_e = 0ull;
+    }
+    if (heads == 1u) {  // one slot for the whole warp: plain warp reductions
+        t.cnt = int(__reduce_add_sync(kFull, unsigned(t.cnt)));
+        t.lo_x = redux_min_u64(kFull, t.lo_x);
+        t.hi_x = redux_max_u64(kFull, t.hi_x);
+        t.lo_e = redux_min_u64(kFull, t.lo_e);
+        t.hi_e = redux_max_u64(kFull, t.hi_e);
+    } else {
+        const unsigned above = heads & ~((2u << lane) - 1u);  // heads past this lane
+        const int last = above ? __ffs(above) - 2 : 31;       // the last lane of this lane's run
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int c = __shfl_down_sync(kFull, t.cnt, d);
+            const unsigned long long a0 = __shfl_down_sync(kFull, t.lo_x, d), a1 = __shfl_down_sync(kFull, t.hi_x, d);
+            const unsigned long long a2 = __shfl_down_sync(kFull, t.lo_e, d), a3 = __shfl_down_sync(kFull, t.hi_e, d);
+            if (lane + d <= last) {
+                t.cnt += c;
+                t.lo_x = a0 < t.lo_x ? a0 : t.lo_x;
+                t.hi_x = a1 > t.hi_x ? a1 : t.hi_x;
+                t.lo_e = a2 < t.lo_e ? a2 : t.lo_e;
+                t.hi_e = a3 > t.hi_e ? a3 : t.hi_e;
+            }
+        }
+    }
+    if (head && r.key >= 0) run_flush(t, cnt, bnd);
 }
 
 __global__ void k_root_init(ClusterPtrs c, int* rcnt) {
     const int k = threadIdx.x;
+    if (k == 6) rcnt[6] = 0;  // OR of every cluster's first slot (the sort key's common zero bits)
     if (k < 6) {
         rcnt[k] = 0;
         c.bnd[4 * k + 0] = ~0ull;
@@ -696,7 +730,7 @@ __global__ void __launch_bounds__(kRunThreads)
 
 // The six roots (:71-82): ranges in face order, face squares, shrunk bounds, centres and
 // split decisions; level 0's descriptor; the roots' quadrant accumulators.
-__global__ void k_root_geom(ClusterPtrs c, const int* rcnt, bool shrink, int n0, LevelDesc* lev, int* scnt,
+__global__ void k_root_geom(ClusterPtrs c, int* rcnt, bool shrink, int n0, LevelDesc* lev, int* scnt,
                             unsigned long long* sbnd) {
     __shared__ int nsp;
     const int k = threadIdx.x;
@@ -709,6 +743,7 @@ __global__ void k_root_geom(ClusterPtrs c, const int* rcnt, bool shrink, int n0,
         c.depth[k] = 0;
         c.begin[k] = b;
         c.end[k] = b + rcnt[k];
+        if (rcnt[k] > 0) atomicOr(&rcnt[6], b);
         c.parent[k] = -1;
         c.nchild[k] = 0;
         c.child[k] = make_int4(-1, -1, -1, -1);
@@ -827,10 +862,11 @@ __global__ void __launch_bounds__(kAllocThreads)
 
 __global__ void k_alloc_fill(int d, LevelDesc* lev, ClusterPtrs c, const int* __restrict__ scnt, int* scnt_w,
                              unsigned long long* sbnd, const int* __restrict__ cbase, int* qchild, bool shrink,
-                             int n0) {
+                             int n0, int* orb) {
     const LevelDesc L = lev[d];
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     bool sp = false;
+    int ob = 0;  // this child's first slot, for the OR of all of them
     if (L.nsplit > 0 && !lev[d + 1].ovf && g < 4 * L.cnt) {
         const int f = g >> 2, q = g & 3, id = L.first + f;
         if (c.split[id]) {
@@ -862,6 +898,7 @@ __global__ void k_alloc_fill(int d, LevelDesc* lev, ClusterPtrs c, const int* __
                 c.depth[cid] = c.depth[id] + 1;
                 c.begin[cid] = acc;
                 c.end[cid] = acc + cq[q];
+                ob = acc;
                 c.parent[cid] = id;
                 c.nchild[cid] = 0;
                 c.child[cid] = make_int4(-1, -1, -1, -1);
@@ -886,6 +923,8 @@ __global__ void k_alloc_fill(int d, LevelDesc* lev, ClusterPtrs c, const int* __
     }
     const unsigned b = __ballot_sync(0xffffffffu, sp);
     if (b && (threadIdx.x & 31) == 0) atomicAdd(&lev[d + 1].nsplit, __popc(b));
+    const unsigned o = __reduce_or_sync(0xffffffffu, unsigned(ob));
+    if (o && (threadIdx.x & 31) == 0) atomicOr(orb, int(o));
 }
 
 // Final labels -> sort keys (the leaf's first tree-order slot).
@@ -1384,11 +1423,12 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
             CSFS_LAUNCH_CHECK();
             k_alloc_fill<<<ceil_div(4 * fbound[k - d], kThreads), kThreads, 0, s>>>(k, lev, c, sc.scnt, sc.scnt,
                                                                                  sc.sbnd, sc.cbase, sc.qchild,
-                                                                                 shrink, n0);
+                                                                                 shrink, n0, sc.rcnt.p + 6);
             CSFS_LAUNCH_CHECK();
         }
         CSFS_CK(cudaMemcpyAsync(sc.host + kHostLev, sc.lev.p, (d_end + 2) * sizeof(LevelDesc),
                                 cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaMemcpyAsync(sc.host + kHostRoots + 6, sc.rcnt.p + 6, sizeof(int), cudaMemcpyDeviceToHost, s));
         CSFS_CK(cudaStreamSynchronize(s));
         for (int k = d; k <= d_end + 1; ++k)
             if (hl[k].ovf) throw std::runtime_error("cluster tree build: capacity bound violated");
@@ -1413,7 +1453,11 @@ void build_tree(DeviceTree& t, Scratch& sc, const double* xyz, const double* w_i
     CSFS_LAUNCH_CHECK();
     int bits = 1;
     while (bits < 31 && (1LL << bits) < n) ++bits;
-    const int* sorted = radix_sort_positions(n, bits, sc.key, sc.kb, sc.vb, sc.sorted, sc.hist, sc.tiles, sc.grand, s);
+    // the keys are clusters' first slots: the low bits that are zero in every one of them
+    // (8 on the L10 grid with 256-particle leaves) need no radix pass
+    const unsigned orb = unsigned(sc.host[kHostRoots + 6]);
+    const int low = orb ? std::min(__builtin_ctz(orb), bits - 1) : 0;
+    const int* sorted = radix_sort_positions(n, bits, sc.key, sc.kb, sc.vb, sc.sorted, sc.hist, sc.tiles, sc.grand, s, low);
     k_gather_tree<<<gp, kThreads, 0, s>>>(n, sorted, sc.fxi, sc.feta, xyz, t.perm, t.xi, t.eta, t.px, t.py, t.pz);
     CSFS_LAUNCH_CHECK();
     finish_tree(t, w_in, n, cheb, s, w_ready);
