@@ -242,6 +242,49 @@ __device__ __forceinline__ void mid_half(double a0, double a1, double& mid, doub
     half = __dmul_rn(0.5, __dsub_rn(a1, a0));
 }
 
+// Both transfer matrices of one (parent, child) pair with a whole thread group at work:
+// At[r*np + k] = L^parent_k(child node r) for the xi axis (rows r < np: Ax) and the eta axis
+// (rows np .. 2np-1: Ae = At + np*np).  The same operations as transfer_cols / bary1d, bit for
+// bit — one division per entry in parallel, each row's denominator summed in node order by
+// one thread — instead of 2np threads each walking a row of np divisions while the others
+// wait (the barrier stalls of k_l2l / k_m2m4, ncu round 2).  EVERY thread of the CTA calls it
+// (four CTA barriers); `active`: the thread's group has a pair; lt, nthr: the thread's index
+// in its group and the group size; aux: 2np doubles, hit: 2np ints of shared memory per group.
+__device__ __forceinline__ void transfer_pair(const Cheb& cheb, bool active, int lt, int nthr, double pxm, double pxh,
+                                              double pem, double peh, double cxm, double cxh, double cem, double ceh,
+                                              double* At, double* aux, int* hit) {
+    const int np = cheb.np;
+    if (active && lt < 2 * np) {  // the child nodes in the parent's reference interval
+        const bool xa = lt < np;
+        const int m = xa ? lt : lt - np;
+        const double node = __dadd_rn(xa ? cxm : cem, __dmul_rn(xa ? cxh : ceh, cheb.nodes[m]));
+        const double ph = xa ? pxh : peh;
+        aux[lt] = ph > 0.0 ? __ddiv_rn(__dsub_rn(node, xa ? pxm : pem), ph) : 0.0;
+        hit[lt] = np;
+    }
+    __syncthreads();
+    if (active)
+        for (int o = lt; o < 2 * np * np; o += nthr) {
+            const int r = o / np, k = o - r * np;
+            const double d = __dsub_rn(aux[r], cheb.nodes[k]);
+            if (fabs(d) < kNodeTol) atomicMin(&hit[r], k);  // the first node hit (interpolation.cpp:28-33)
+            At[o] = __ddiv_rn(cheb.weights[k], d);
+        }
+    __syncthreads();
+    if (active && lt < 2 * np && hit[lt] == np) {
+        double denom = 0.0;
+        for (int k = 0; k < np; ++k) denom = __dadd_rn(denom, At[lt * np + k]);
+        aux[lt] = __ddiv_rn(1.0, denom);
+    }
+    __syncthreads();
+    if (active)
+        for (int o = lt; o < 2 * np * np; o += nthr) {
+            const int r = o / np, k = o - r * np, h = hit[r];
+            At[o] = h < np ? (k == h ? 1.0 : 0.0) : __dmul_rn(At[o], aux[r]);
+        }
+    __syncthreads();
+}
+
 // M2M (cluster_tree.cpp:192-216): pw = sum_children Axi * cw * Aeta^T, for one level.
 __global__ void __launch_bounds__(kPassThreads)
     k_m2m(TreeView t, Cheb cheb, int first, double* __restrict__ qw, int mode, Own own) {
@@ -293,8 +336,9 @@ __global__ void __launch_bounds__(kPassThreads)
 // The same M2M with the (up to) four children in parallel: thread group q (kPassThreads
 // threads) builds child q's transfer matrices and its contribution Axi cw Aeta^T into
 // shared memory; the contributions are then added in child order — the same operations
-// and order as k_m2m, bit for bit, with 3 barriers per cluster instead of 12.  Used while
-// 16 (p+1)^2 doubles fit the 48 KB static window (degree <= 18).
+// and order as k_m2m, bit for bit, with 6 barriers per cluster instead of 12 and the
+// transfer matrices built by the whole group (transfer_pair).  Used while 16 (p+1)^2 +
+// 16 (p+1) doubles fit the 48 KB static window (degree <= 17).
 constexpr int kM2mGroups = 4;
 __global__ void __launch_bounds__(kM2mGroups * kPassThreads)
     k_m2m4(TreeView t, Cheb cheb, int first, double* __restrict__ qw, int mode, Own own) {
@@ -308,6 +352,7 @@ __global__ void __launch_bounds__(kM2mGroups * kPassThreads)
     double* Ae = Ax + npp;
     double* tmp = Ae + npp;  // tmp[k1*np + m2]
     double* contrib = sm + kM2mGroups * 3 * npp;
+    double* aux = sm + kM2mGroups * 4 * npp + q * 4 * np;  // 2np doubles + 2np ints per group
     double pxm, pxh, pem, peh;
     mid_half(t.xi0[c], t.xi1[c], pxm, pxh);
     mid_half(t.eta0[c], t.eta1[c], pem, peh);
@@ -315,14 +360,13 @@ __global__ void __launch_bounds__(kM2mGroups * kPassThreads)
     const int chs[4] = {ch4.x, ch4.y, ch4.z, ch4.w};
     const bool mine = q < nch;
     const int ch = mine ? chs[q] : 0;
+    double cxm = 0.0, cxh = 0.0, cem = 0.0, ceh = 0.0;
     if (mine) {
-        double cxm, cxh, cem, ceh;
         mid_half(t.xi0[ch], t.xi1[ch], cxm, cxh);
         mid_half(t.eta0[ch], t.eta1[ch], cem, ceh);
-        if (lt < np) transfer_cols(cheb, pxm, pxh, cxm, cxh, lt, Ax);
-        else if (lt < 2 * np) transfer_cols(cheb, pem, peh, cem, ceh, lt - np, Ae);
     }
-    __syncthreads();
+    transfer_pair(cheb, mine, lt, kPassThreads, pxm, pxh, pem, peh, cxm, cxh, cem, ceh, Ax, aux,
+                  reinterpret_cast<int*>(aux + 2 * np));
     if (mine) {
         const double* cw = qw + (long long)ch * npp;
         for (int o = lt; o < npp; o += kPassThreads) {
@@ -365,9 +409,9 @@ __global__ void __launch_bounds__(kPassThreads)
     mid_half(t.eta0[c], t.eta1[c], pem, peh);
     mid_half(t.xi0[ch], t.xi1[ch], cxm, cxh);
     mid_half(t.eta0[ch], t.eta1[ch], cem, ceh);
-    if (threadIdx.x < np) transfer_cols(cheb, pxm, pxh, cxm, cxh, threadIdx.x, Ax);
-    else if (threadIdx.x < 2 * np) transfer_cols(cheb, pem, peh, cem, ceh, threadIdx.x - np, Ae);
-    __syncthreads();
+    double* aux = tmp + npp * dim;  // 2np doubles + 2np ints
+    transfer_pair(cheb, true, threadIdx.x, kPassThreads, pxm, pxh, pem, peh, cxm, cxh, cem, ceh, Ax, aux,
+                  reinterpret_cast<int*>(aux + 2 * np));
     const double* P = qphi + (long long)c * npp * dim;
     for (int o = threadIdx.x; o < npp * dim; o += kPassThreads) {
         const int d = o % dim, r = o / dim, n1 = r / np, m2 = r % np;
@@ -480,7 +524,7 @@ void upward_pass(DeviceTree& src, const Cheb& cheb, cudaStream_t s, int mode, Ow
     }
     CSFS_LAUNCH_CHECK();
     const size_t sm_m2m = size_t(3) * npp * sizeof(double);
-    const size_t sm_m2m4 = size_t(4 * kM2mGroups) * npp * sizeof(double);
+    const size_t sm_m2m4 = size_t(4 * kM2mGroups) * (npp + np) * sizeof(double);
     const int lo = mode == 1 ? 1 : 0;
     const int hi = mode == 2 ? 0 : src.depth_max() - 1;
     for (int L = hi; L >= lo; --L) {
@@ -498,7 +542,7 @@ void downward_pass(DeviceTree& tgt, const Cheb& cheb, int dim, const double* phi
                    cudaStream_t s, Own own, bool out_perm) {
     const TreeView v = tgt.view();
     const int np = cheb.np, npp = np * np;
-    const size_t sm_l2l = size_t(2 * npp + npp * dim) * sizeof(double);
+    const size_t sm_l2l = size_t(2 * npp + npp * dim + 4 * np) * sizeof(double);
     for (int L = 1; L <= tgt.depth_max(); ++L) {
         if (tgt.level_count[L] == 0) continue;
         k_l2l<<<tgt.level_count[L], kPassThreads, sm_l2l, s>>>(v, cheb, tgt.level_first[L], dim, tgt.qphi, own);
