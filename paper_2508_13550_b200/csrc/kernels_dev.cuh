@@ -100,22 +100,32 @@ __device__ __forceinline__ double li2_bernoulli(double z) {
 // C = false (the provably far entries, whose u already carries the fused form's few-ulp
 // absolute difference): z = -log(t) without the compensation term, which only corrects t's
 // own rounding (<= 2^-53 absolutely) — 4 FP64 instructions and a MUFU fewer.
+// Branch-free: both regions run the same instructions on selected operands — the log of
+// a = (u > 1/2 ? u : 1 - u) gives z, the second log is ln(1 - u) for the reflection term
+// (of 1.0 below 1/2: exactly 0, unused) — because a data-dependent branch around every
+// evaluation (BSSY / BRA / BSYNC) keeps the compiler from interleaving the independent
+// evaluations of a source batch: the biharmonic loops then ran one dependent FP64 chain at
+// a time per warp (41% FP64 pipe, "wait" the top stall, ncu round 2).  Nearly every
+// evaluation has u > 1/2 (x.y > 0: all PP / CP and the deep CC entries), which needed both
+// logs before too; the few below 1/2 now pay a second log.
 template <bool C = true>
 __device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
     constexpr double kPi2Over6 = kPi * kPi / 6.0;
-    if (u > 0.5) {
-        const double y = 1.0 - u;  // exact (Sterbenz)
-        const double lu = fast_log(u, tab);
-        const double ly = fast_log(y, tab);  // y == 0 only when u == 1 (selected away)
-        const double r = kPi2Over6 - lu * ly - li2_bernoulli(-lu);
-        return (u == 1.0) ? kPi2Over6 : r;
+    const bool hi = u > 0.5;
+    const double t = 1.0 - u;  // exact for u > 1/2 (Sterbenz); 0 only when u == 1 (selected away)
+    const double la = fast_log(hi ? u : t, tab);
+    const double lb = fast_log(hi ? t : 1.0, tab);
+    double z = -la;
+    if (C) {
+        // u <= 1/2: z = -log1p(-u) via the compensated form log(t) - ((t - 1) + u)/t: the
+        // correction (t - 1) + u is t's rounding error (|.| <= 2^-53), so the bare MUFU
+        // reciprocal (2^-20) is enough — it moves z by < 2^-72
+        const double zc = -(la - ((t - 1.0) + u) * rcp_seed(t));
+        z = hi ? z : zc;
     }
-    // z = -log1p(-u) via the compensated form log(t) - ((t - 1) + u)/t, t = 1 - u: the
-    // correction (t - 1) + u is t's rounding error (|.| <= 2^-53), so the bare MUFU
-    // reciprocal (2^-20) is enough — it moves z by < 2^-72
-    const double t = 1.0 - u;
-    const double z = C ? -(fast_log(t, tab) - ((t - 1.0) + u) * rcp_seed(t)) : -fast_log(t, tab);
-    return li2_bernoulli(z);
+    const double li = li2_bernoulli(z);
+    const double r = kPi2Over6 - la * lb - li;  // the reflection Li2(u) = pi^2/6 - ln u ln(1-u) - Li2(1-u)
+    return hi ? ((u == 1.0) ? kPi2Over6 : r) : li;
 }
 
 // BiharmonicOp: dilog(u) / 4pi, u = min(1, (1 + x.y)/2).  Targets enter halved (exact), so
