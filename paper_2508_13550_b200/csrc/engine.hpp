@@ -54,9 +54,11 @@ struct DevBuf {
 // (negative = proxy points), bit 30 of the magnitude (the coincidence guard is needed
 // for this entry; kernels_dev.cuh eval<G>) and bit 29 (the fused 1 - x.y is safe, eval<.., F>).
 constexpr int kSegGuard = 1 << 30;
-// bit 29: the entry's point sets are more than kFuseGap apart — the fused 1 - x.y may be used
+// bit 29: the entry's point sets are more than kFuseGap and less than kFuseMaxDist apart — the
+// fused 1 - x.y may be used, and x.y > 0 for every pair
 constexpr int kSegFused = 1 << 29;
 constexpr double kFuseGap = 4.48e-3;  // chordal; 1 - x.y >= kFuseGap^2 / 2 >= 1.0e-5
+constexpr double kFuseMaxDist = 1.41;  // chordal; x.y >= 1 - kFuseMaxDist^2 / 2 = 5.9e-3: one hemisphere
 __host__ __device__ __forceinline__ int seg_len(int y) { return (y < 0 ? -y : y) & (kSegFused - 1); }
 __host__ __device__ __forceinline__ bool seg_guard(int y) { return ((y < 0 ? -y : y) & kSegGuard) != 0; }
 __host__ __device__ __forceinline__ bool seg_fused(int y) { return ((y < 0 ? -y : y) & kSegFused) != 0; }

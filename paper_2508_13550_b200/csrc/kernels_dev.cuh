@@ -128,6 +128,16 @@ __device__ __forceinline__ double dilog_dev(double u, const LogTable& tab) {
     return hi ? ((u == 1.0) ? kPi2Over6 : r) : li;
 }
 
+// The provably far entries (kSegFused: every pair within one hemisphere and > kFuseGap apart,
+// so 1/2 + 2.9e-3 <= u <= 1 - 5e-6): always the reflection region, no select, no clamp, no
+// u == 1 case — bit for bit what dilog_dev<false> returns there.
+__device__ __forceinline__ double dilog_far(double u, const LogTable& tab) {
+    constexpr double kPi2Over6 = kPi * kPi / 6.0;
+    const double la = fast_log(u, tab);
+    const double lb = fast_log(1.0 - u, tab);  // 1 - u exact (Sterbenz)
+    return kPi2Over6 - la * lb - li2_bernoulli(-la);
+}
+
 // BiharmonicOp: dilog(u) / 4pi, u = min(1, (1 + x.y)/2).  Targets enter halved (exact), so
 // the reference's 0.5 (1 + x.y) is 0.5 + t'.s bit for bit (scaling by 2 commutes with the
 // roundings): unfused in the reference's order, one DMUL fewer.  On the provably far entries
@@ -151,12 +161,15 @@ struct OpBiharmonic {
     template <bool G = true, bool F = false>  // regular at coincidence: no guard either way
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
-        K[0] = dilog_dev<!F>(u_of<F>(tx, ty, tz, sx, sy, sz), tab);
+        K[0] = F ? dilog_far(fma(tz, sz, fma(ty, sy, fma(tx, sx, 0.5))), tab)
+                 : dilog_dev<true>(u_of<false>(tx, ty, tz, sx, sy, sz), tab);
     }
     template <bool G = true, bool F = false>
     __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
                                          double* acc, const LogTable& tab) const {
-        acc[0] = fma(sw, dilog_dev<!F>(u_of<F>(tx, ty, tz, sx, sy, sz), tab), acc[0]);
+        double K[1];
+        value<G, F>(tx, ty, tz, sx, sy, sz, K, tab);
+        acc[0] = fma(sw, K[0], acc[0]);
     }
     __device__ __forceinline__ void operator()(double tx, double ty, double tz, double sx, double sy,
                                                double sz, double sw, double* acc,

@@ -80,14 +80,18 @@ __device__ __forceinline__ bool needs_guard(const TreeView& T, const TreeView& S
 // every pair of its point sets is more than kFuseGap apart (chordal, bounding spheres with
 // the particle / proxy radii): then 1 - x.y >= kFuseGap^2/2 = 1e-5 and the fused form
 // differs from the reference's unfused one by < 8e-11 relatively per pair (worst case).
-// Unit vectors only (the distance bound uses |x| = 1).
+// Unit vectors only (the distance bound uses |x| = 1).  The entry must also lie within one
+// hemisphere — every pair less than kFuseMaxDist = 1.41 apart, so x.y >= 1 - 1.41^2/2 =
+// 5.9e-3 > 0: the biharmonic functor's far form then knows u = (1 + x.y)/2 > 1/2 and runs
+// the dilogarithm's reflection region without a select (kernels_dev.cuh dilog_far).  Only
+// the few top-level CC entries between opposite faces fail it (0.1% of C5's evaluations).
 __device__ __forceinline__ bool can_fuse(const TreeView& T, const TreeView& S, int t, bool t_prox, int s,
                                          bool s_prox) {
     if (*T.off_sphere || *S.off_sphere) return false;
     const double dx = T.cx[t] - S.cx[s], dy = T.cy[t] - S.cy[s], dz = T.cz[t] - S.cz[s];
     const double R = sqrt(dx * dx + dy * dy + dz * dz);
     const double rt = t_prox ? T.qrad[t] : T.rad[t], rs = s_prox ? S.qrad[s] : S.rad[s];
-    return R - rt - rs > kFuseGap;
+    return R - rt - rs > kFuseGap && R + rt + rs < kFuseMaxDist;
 }
 
 // A target cluster is ours when the range is everything, it is at depth 0 (every rank
