@@ -133,16 +133,23 @@ __global__ void __launch_bounds__(kIB, MinBlocksOf<Op>::value) k_interact(Intera
     double* const red = D == 1 ? reinterpret_cast<double*>(sbuf) : red_own;
     static_assert(D != 1 || kIB * kTPT * sizeof(double) <= sizeof(double2) * 2 * kICH, "red fits the source buffers");
     extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
-    __shared__ int item_sh;
+    __shared__ int item_sh[2];
     const int tid = threadIdx.x;
     const LogTable tab = stage_log_table(tab_sm, P.log_tab);  // synced by the loop's first barrier
+    // The queue ticket of the NEXT item is fetched while this one is evaluated (the atomic's
+    // round trip sat at the head of every item: 16% of the stall samples of the small-leaf
+    // configs, ncu round 2).  Two slots: thread 0 publishes ticket i + 1 into the slot that
+    // nobody reads until the next barrier, so one barrier per item is enough.
+    int ticket = 0, slot = 0;
+    if (tid == 0) ticket = atomicAdd(P.counter, 1);
     for (;;) {
-        if (tid == 0) item_sh = atomicAdd(P.counter, 1);
-        __syncthreads();
-        const int q = item_sh;
-        __syncthreads();
+        if (tid == 0) item_sh[slot] = ticket;
+        __syncthreads();  // also: the previous item's shared-memory reads are done
+        const int q = item_sh[slot];
+        slot ^= 1;
         const int n_items = P.n_own ? *P.n_own : P.n_items;
         if (q >= n_items) break;
+        if (tid == 0) ticket = atomicAdd(P.counter, 1);
 #ifndef CSFS_ITEM_ORDER_REVERSED
 #define CSFS_ITEM_ORDER_REVERSED 1
 #endif
@@ -374,15 +381,18 @@ __global__ void __launch_bounds__(kIB, CSFS_MMINB) k_mutual(MutualParams P, Op o
     __shared__ double colbuf[kIB / 32][kICH];
     __shared__ double red[kIB * kMTPT];
     extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
-    __shared__ int pair_sh;
+    __shared__ int pair_sh[2];
     const int tid = threadIdx.x, lane = tid & 31;
     const LogTable tab = stage_log_table(tab_sm, P.log_tab);  // synced by the loop's first barrier
+    int ticket = 0, slot = 0;  // the next pair's queue ticket, fetched a pair ahead (see k_interact)
+    if (tid == 0) ticket = atomicAdd(P.counter, 1);
     for (;;) {
-        if (tid == 0) pair_sh = atomicAdd(P.counter, 1);
+        if (tid == 0) pair_sh[slot] = ticket;
         __syncthreads();  // also: the previous pair's shared-memory reads are done
-        const int pq = pair_sh;
-        __syncthreads();
+        const int pq = pair_sh[slot];
+        slot ^= 1;
         if (pq >= (P.n_own ? *P.n_own : P.n_pairs)) break;
+        if (tid == 0) ticket = atomicAdd(P.counter, 1);
         const int p = P.idx ? P.idx[pq] : pq;
         if (P.anchor) {
             const long long a = P.anchor[p];
