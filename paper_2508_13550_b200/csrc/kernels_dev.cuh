@@ -97,9 +97,9 @@ __device__ __forceinline__ double li2_bernoulli(double z) {
     return fma(w, fma(z, p, -0.25), z);
 }
 
-// C = false (the provably far entries, whose u already carries the fused form's few-ulp
-// absolute difference): z = -log(t) without the compensation term, which only corrects t's
-// own rounding (<= 2^-53 absolutely) — 4 FP64 instructions and a MUFU fewer.
+// C = false: z = -log(t) without the compensation term, which only corrects t's own
+// rounding (<= 2^-53 absolutely) — 4 FP64 instructions and a MUFU fewer (kept for A/B; the
+// kernels use C = true here and dilog_far on the provably far entries).
 // Branch-free: both regions run the same instructions on selected operands — the log of
 // a = (u > 1/2 ? u : 1 - u) gives z, the second log is ln(1 - u) for the reflection term
 // (of 1.0 below 1/2: exactly 0, unused) — because a data-dependent branch around every
@@ -145,24 +145,30 @@ __device__ __forceinline__ double dilog_far(double u, const LogTable& tab) {
 // which moves the kernel by <= |dilog'(u)| 4e-16 = |ln(1 - u)/u| 4e-16 <= 5e-15 absolutely
 // (1 - u >= 5e-6 there) — u = (1 + x.y)/2 has no near-coincidence cancellation to
 // preserve.  The symmetric kernel keeps K(t, s) = K(s, t) bit for bit (exact products commute).
+#ifndef CSFS_BIH_MINB
+#define CSFS_BIH_MINB 3
+#endif
+#ifndef CSFS_BIH_UNROLL
+#define CSFS_BIH_UNROLL 8
+#endif
 struct OpBiharmonic {
-    static constexpr int kMinBlocks = 3;
+    static constexpr int kMinBlocks = CSFS_BIH_MINB;
     static constexpr bool kFusable = true;  // has a fused form (u from three FMAs)
     static constexpr int dim = 1;
-    static constexpr int kUnroll = 4;
+    static constexpr int kUnroll = CSFS_BIH_UNROLL;
     static constexpr double kSym = 1.0;
     __device__ __forceinline__ static double tgt(double x) { return 0.5 * x; }
     __device__ __forceinline__ double scale() const { return kInv4Pi; }
-    template <bool F>
-    __device__ __forceinline__ static double u_of(double tx, double ty, double tz, double sx, double sy, double sz) {
-        const double u0 = F ? fma(tz, sz, fma(ty, sy, fma(tx, sx, 0.5))) : __dadd_rn(0.5, dot_ref(tx, ty, tz, sx, sy, sz));
+    // the reference's u = min(1, 0.5 (1 + x.y)), unfused, in its order
+    __device__ __forceinline__ static double u_ref(double tx, double ty, double tz, double sx, double sy, double sz) {
+        const double u0 = __dadd_rn(0.5, dot_ref(tx, ty, tz, sx, sy, sz));
         return (u0 < 1.0) ? u0 : 1.0;  // std::min(1.0, u0)
     }
     template <bool G = true, bool F = false>  // regular at coincidence: no guard either way
     __device__ __forceinline__ void value(double tx, double ty, double tz, double sx, double sy, double sz,
                                           double* K, const LogTable& tab) const {
         K[0] = F ? dilog_far(fma(tz, sz, fma(ty, sy, fma(tx, sx, 0.5))), tab)
-                 : dilog_dev<true>(u_of<false>(tx, ty, tz, sx, sy, sz), tab);
+                 : dilog_dev<true>(u_ref(tx, ty, tz, sx, sy, sz), tab);
     }
     template <bool G = true, bool F = false>
     __device__ __forceinline__ void eval(double tx, double ty, double tz, double sx, double sy, double sz, double sw,
