@@ -8,7 +8,8 @@
 //   separated and big (count > n0)  -> PC: the cluster's (p+1)^2 proxy points/weights
 //   not separated, internal         -> descend
 //   otherwise (separated small, or non-separated leaf) -> PP: the cluster's particles
-// evaluated with the same kernel functors and shared-memory log table as the FMM.
+// evaluated with the same kernel functors and shared-memory log table as the FMM (staged
+// per CTA).
 // Targets are processed in source-tree order when targets == sources, so the 32 lanes of
 // a warp (neighbours on the sphere) traverse almost identically (little divergence).
 #include "engine.hpp"
@@ -18,7 +19,11 @@ namespace csfs_b200 {
 
 namespace {
 
-constexpr int kCstcThreads = 128;
+#ifndef CSFS_CSTC_UNROLL
+#define CSFS_CSTC_UNROLL 4
+#endif
+constexpr int kCstcUnroll = CSFS_CSTC_UNROLL;
+constexpr int kCstcThreads = 256;  // 3 CTAs (3 x 64 KB log table) per SM
 constexpr int kStack = 4 * kMaxDepth + 8;
 
 template <class Op>
@@ -27,7 +32,10 @@ __global__ void __launch_bounds__(kCstcThreads)
            const double* __restrict__ sw, const double* __restrict__ qw, double mac, int n0, Op op,
            const double2* __restrict__ log_tab, double* __restrict__ out, unsigned long long* counts) {
     constexpr int D = Op::dim;
-    const LogTable tab{log_tab};  // read through L1 (many small CTAs: no per-CTA staging)
+    // the log table staged in shared memory like the FMM kernels (random 16-byte gathers
+    // through L1 cost a sector per lane)
+    extern __shared__ double2 tab_sm[];  // kLogTabBytes (dynamic)
+    const LogTable tab = stage_log_table(tab_sm, log_tab);
     __syncthreads();
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long npp_ = 0, npc = 0;
@@ -53,6 +61,7 @@ __global__ void __launch_bounds__(kCstcThreads)
             if (sep) {
                 if (e - b > n0) {
                     const long long q0 = (long long)s * npp;
+#pragma unroll kCstcUnroll
                     for (int k = 0; k < npp; ++k) op(tx, ty, tz, S.qx[q0 + k], S.qy[q0 + k], S.qz[q0 + k], qw[q0 + k], acc, tab);
                     ++npc;
                     continue;
@@ -63,6 +72,7 @@ __global__ void __launch_bounds__(kCstcThreads)
                 for (int q = 0; q < S.nchild[s] && sp < kStack; ++q) stack[sp++] = cs[q];
                 continue;
             }
+#pragma unroll kCstcUnroll
             for (int j = b; j < e; ++j) op(tx, ty, tz, S.px[j], S.py[j], S.pz[j], sw[j], acc, tab);
             ++npp_;
         }
@@ -91,8 +101,10 @@ void cstc_eval(const KernelSpec& k, const double* txyz, long long nt, const int*
     CSFS_CK(cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), s));
     const TreeView S = src.view();
     with_op(k, [&](auto op) {
-        k_cstc<<<ceil_div(nt, kCstcThreads), kCstcThreads, 0, s>>>(txyz, nt, order, S, src.w, src.qw, mac, n0, op,
-                                                                    log_tab, out, counts);
+        auto kern = k_cstc<decltype(op)>;
+        CSFS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLogTabBytes)));
+        kern<<<ceil_div(nt, kCstcThreads), kCstcThreads, kLogTabBytes, s>>>(txyz, nt, order, S, src.w, src.qw, mac, n0, op,
+                                                                            log_tab, out, counts);
         CSFS_LAUNCH_CHECK();
     });
 }
