@@ -57,3 +57,29 @@ def test_cstc_targets_differ_and_full_size(engine):
     print(f"C2 CSTC: GPU {st.t_total*1e3:.1f} ms, rel L2 {rel_l2(g, r):.2e}")
     assert rel_l2(g, r) < 1e-10
     assert (st.pp, st.pc) == (int(rst[5]), int(rst[6]))
+
+
+@pytest.mark.parametrize("kname", ["laplace", "biharmonic", "biot_savart", "sal"])
+def test_cstc_warp_traversal_equals_per_target_traversal(engine, kname, monkeypatch):
+    """The warp-cooperative traversal (shared stack of (cluster, lane mask), sources staged
+    once per warp) sums every target in the order of its own depth-first traversal: bit for
+    bit the one-thread-per-target kernel (CSFS_B200_CSTC=thread), same counts — on a grid
+    (targets == sources, tree order), on shuffled separate targets (sparse lane masks) and on
+    a target count that is not a multiple of 32."""
+    xyz, a = ref.grid("cubed_sphere", 5)
+    w = ref.sph_harm(4, 3, xyz) * a
+    rng = np.random.default_rng(11)
+    tx = xyz[rng.permutation(len(xyz))[:3001]] * 1.0
+    k = Kernel.parse(kname)
+    cfg = TraversalConfig(method=Method.Cstc, mac=0.6, degree=8, n0=40)
+    for tgt in (ParticleSet(xyz, w), ParticleSet(tx, np.zeros(len(tx)))):
+        res = {}
+        for mode in ("thread", "warp"):
+            if mode == "thread":
+                monkeypatch.setenv("CSFS_B200_CSTC", "thread")
+            else:
+                monkeypatch.delenv("CSFS_B200_CSTC", raising=False)
+            st = SumStats()
+            res[mode] = (engine.summed_potential(tgt, ParticleSet(xyz, w), k, cfg, st).values.copy(), st.pp, st.pc)
+        assert res["thread"][1:] == res["warp"][1:]
+        assert np.array_equal(res["thread"][0].view(np.uint64), res["warp"][0].view(np.uint64))
