@@ -140,10 +140,14 @@ __global__ void __launch_bounds__(kCstcWarpThreads, 2)
     int sp = 6;
     __syncwarp();
     const int npp = S.npp;
+    const bool unit = order != nullptr && !*S.off_sphere;  // targets are the tree's particles, all on the sphere
 
-    // `act` lanes add the cnt sources at X/Y/Z/W[base ..) to their sums, in index order
+    // `act` lanes add the cnt sources at X/Y/Z/W[base ..) to their sums, in index order.
+    // guard (warp-uniform): some active lane may hold a pair with 1 - x.y < 1e-14; without it
+    // the functor's coincidence guard is compiled out — the same values (the guard only
+    // drops coincident pairs), fewer integer instructions.
     auto evaluate = [&](const double* __restrict__ X, const double* __restrict__ Y, const double* __restrict__ Z,
-                        const double* __restrict__ W, long long base, int cnt, bool act) {
+                        const double* __restrict__ W, long long base, int cnt, bool act, bool guard) {
         double nx = 0.0, ny = 0.0, nz = 0.0, nw = 0.0;
         if (lane < cnt) {
             nx = X[base + lane];
@@ -164,11 +168,17 @@ __global__ void __launch_bounds__(kCstcWarpThreads, 2)
                 nw = W[base + j];
             }
             const int m = min(32, cnt - c0);
-            if (act) {
+            if (act && guard) {
 #pragma unroll 4
                 for (int k = 0; k < m; ++k) {
                     const double2 a = sxy[k], b = szw[k];
-                    op(tx, ty, tz, a.x, a.y, b.x, b.y, acc, tab);
+                    op.template eval<true, false>(tx, ty, tz, a.x, a.y, b.x, b.y, acc, tab);
+                }
+            } else if (act) {
+#pragma unroll 4
+                for (int k = 0; k < m; ++k) {
+                    const double2 a = sxy[k], b = szw[k];
+                    op.template eval<false, false>(tx, ty, tz, a.x, a.y, b.x, b.y, acc, tab);
                 }
             }
         }
@@ -190,6 +200,11 @@ __global__ void __launch_bounds__(kCstcWarpThreads, 2)
         const bool pp = in && !pc && !down;
         const unsigned mdown = __ballot_sync(kFull, down);
         const unsigned mpc = __ballot_sync(kFull, pc), mpp = __ballot_sync(kFull, pp);
+        // free of coincident pairs: the target is more than 1e-6 outside the sphere that holds
+        // the proxies / the particles (the guard triggers below ~1.4e-7; unit vectors only —
+        // known for the tree's own particles, so only when targets == sources)
+        const bool gpc = !unit || !(R - S.qrad[s] > 1e-6), gpp = !unit || !(R - S.rad[s] > 1e-6);
+        const bool guard_pc = __ballot_sync(kFull, pc && gpc) != 0, guard_pp = __ballot_sync(kFull, pp && gpp) != 0;
         __syncwarp();  // every lane has read this entry before its slot is overwritten
         if (mdown && sp + nch <= kStack) {  // the children in quadrant order (popped last to first)
             const int4 ch = S.child[s];
@@ -198,11 +213,11 @@ __global__ void __launch_bounds__(kCstcWarpThreads, 2)
             sp += nch;
         }
         if (mpc) {
-            evaluate(S.qx, S.qy, S.qz, qw, (long long)s * npp, npp, pc);
+            evaluate(S.qx, S.qy, S.qz, qw, (long long)s * npp, npp, pc, guard_pc);
             npc += pc ? 1 : 0;
         }
         if (mpp) {
-            evaluate(S.px, S.py, S.pz, sw, b, e - b, pp);
+            evaluate(S.px, S.py, S.pz, sw, b, e - b, pp, guard_pp);
             npp_ += pp ? 1 : 0;
         }
         __syncwarp();  // the pushes are visible to the next pop
