@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <thread>
 #include <memory>
 #include <string>
 #include <vector>
@@ -165,6 +166,10 @@ void free_context(csfs_b200_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->sc.host) cudaFreeHost(c->sc.host);
+    for (int b = 0; b < 2; ++b) {
+        if (c->stage_pin[b]) cudaFreeHost(c->stage_pin[b]);
+        if (c->stage_ev[b]) cudaEventDestroy(c->stage_ev[b]);
+    }
     if (c->own) cudaStreamDestroy(c->own);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->hi) cudaStreamDestroy(c->hi);
@@ -458,6 +463,112 @@ const DeviceTree& which_tree(const csfs_b200_ctx* c, int which) {
 
 }  // namespace
 
+namespace {
+
+// ---- pageable caller buffers ---------------------------------------------------------------
+// cudaMemcpyAsync from / to pageable memory goes through the driver's staging buffer with a
+// single-threaded copy (~12 GB/s here: 251 MB of C5 inputs and results cost 17 ms more than
+// from pinned memory).  The host-pointer csfmm stages such buffers itself: a few host threads
+// copy 32 MB pieces into / out of two pinned bounce buffers while the DMA of the previous piece
+// runs.  Pinned or registered caller memory, small buffers and CSFS_B200_NO_STAGE=1 take the
+// plain cudaMemcpyAsync.  (Page-locking the caller's memory per call is slower than either:
+// INTEGRATION.md.)
+constexpr size_t kStageBytes = size_t(32) << 20;
+constexpr size_t kStageMin = size_t(48) << 20;  // smaller buffers gain nothing (measured: 9 MB slower, 38 MB even)
+
+bool host_pageable(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+void par_memcpy(char* dst, const char* src, size_t bytes) {
+    static const int nthr = [] {
+        const unsigned h = std::thread::hardware_concurrency();
+        return int(std::max(1u, std::min(8u, h / 2)));
+    }();
+    const size_t per = (bytes / size_t(nthr) + 4095) & ~size_t(4095);
+    if (nthr == 1 || per == 0 || bytes < (size_t(2) << 20)) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 1; t < nthr; ++t) {
+        const size_t off = size_t(t) * per;
+        if (off >= bytes) break;
+        const size_t n = std::min(per, bytes - off);
+        th.emplace_back([=] { std::memcpy(dst + off, src + off, n); });
+    }
+    std::memcpy(dst, src, std::min(per, bytes));
+    for (auto& t : th) t.join();
+}
+
+bool stage_ready(csfs_b200_ctx* c) {
+    for (int b = 0; b < 2; ++b) {
+        if (!c->stage_pin[b] && cudaHostAlloc(&c->stage_pin[b], kStageBytes, cudaHostAllocDefault) != cudaSuccess) {
+            (void)cudaGetLastError();
+            c->stage_pin[b] = nullptr;
+            return false;
+        }
+        if (!c->stage_ev[b] && cudaEventCreateWithFlags(&c->stage_ev[b], cudaEventDisableTiming) != cudaSuccess) {
+            (void)cudaGetLastError();
+            c->stage_ev[b] = nullptr;
+            return false;
+        }
+    }
+    return true;
+}
+
+bool want_stage(csfs_b200_ctx* c, const void* host, size_t bytes) {
+    static const bool off = std::getenv("CSFS_B200_NO_STAGE") != nullptr;
+    return !off && bytes >= kStageMin && host_pageable(host) && stage_ready(c);
+}
+
+// host -> device on `s`; returns once the host buffer has been read (the DMA may still run)
+void h2d_staged(csfs_b200_ctx* c, double* dst, const double* src, size_t bytes, cudaStream_t s) {
+    if (!want_stage(c, src, bytes)) {
+        CSFS_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    int b = 0;
+    for (size_t done = 0; done < bytes; b ^= 1) {
+        const size_t n = std::min(kStageBytes, bytes - done);
+        CSFS_CK(cudaEventSynchronize(c->stage_ev[b]));  // the DMA that last used this buffer
+        par_memcpy(static_cast<char*>(c->stage_pin[b]), reinterpret_cast<const char*>(src) + done, n);
+        CSFS_CK(cudaMemcpyAsync(reinterpret_cast<char*>(dst) + done, c->stage_pin[b], n, cudaMemcpyHostToDevice, s));
+        CSFS_CK(cudaEventRecord(c->stage_ev[b], s));
+        done += n;
+    }
+}
+
+// device -> host on `s`; returns with the data in `dst` when it was staged (else the caller
+// synchronizes `s` as before)
+void d2h_staged(csfs_b200_ctx* c, double* dst, const double* src, size_t bytes, cudaStream_t s) {
+    if (!want_stage(c, dst, bytes)) {
+        CSFS_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        return;
+    }
+    auto issue = [&](size_t off, int b) {
+        const size_t n = std::min(kStageBytes, bytes - off);
+        CSFS_CK(cudaEventSynchronize(c->stage_ev[b]));
+        CSFS_CK(cudaMemcpyAsync(c->stage_pin[b], reinterpret_cast<const char*>(src) + off, n, cudaMemcpyDeviceToHost, s));
+        CSFS_CK(cudaEventRecord(c->stage_ev[b], s));
+    };
+    issue(0, 0);
+    int b = 0;
+    for (size_t off = 0; off < bytes; off += kStageBytes, b ^= 1) {
+        if (off + kStageBytes < bytes) issue(off + kStageBytes, b ^ 1);  // the next piece flies meanwhile
+        CSFS_CK(cudaEventSynchronize(c->stage_ev[b]));
+        par_memcpy(reinterpret_cast<char*>(dst) + off, static_cast<const char*>(c->stage_pin[b]),
+                   std::min(kStageBytes, bytes - off));
+    }
+}
+
+}  // namespace
+
 extern "C" {
 
 int csfs_b200_create(csfs_b200_ctx** out, int device) {
@@ -498,11 +609,11 @@ int csfs_b200_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const doubl
         cudaStream_t s = c->own;
         const bool same = (txyz == sxyz && nt == ns);
         c->h_txyz.grow(nt * 3);
-        CSFS_CK(cudaMemcpyAsync(c->h_txyz.p, txyz, nt * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        h2d_staged(c, c->h_txyz.p, txyz, nt * 3 * sizeof(double), s);
         const double* dsrc = c->h_txyz.p;
         if (!same) {
             c->h_sxyz.grow(ns * 3);
-            CSFS_CK(cudaMemcpyAsync(c->h_sxyz.p, sxyz, ns * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+            h2d_staged(c, c->h_sxyz.p, sxyz, ns * 3 * sizeof(double), s);
             dsrc = c->h_sxyz.p;
         }
         c->h_w.grow(ns);
@@ -512,12 +623,12 @@ int csfs_b200_csfmm(csfs_b200_ctx* c, const double* txyz, size_t nt, const doubl
         // the positions by the weights' transfer time)
         CSFS_CK(cudaEventRecord(c->ev[10], s));
         CSFS_CK(cudaStreamWaitEvent(c->aux, c->ev[10], 0));
-        CSFS_CK(cudaMemcpyAsync(c->h_w.p, sw, ns * sizeof(double), cudaMemcpyHostToDevice, c->aux));
+        h2d_staged(c, c->h_w.p, sw, ns * sizeof(double), c->aux);
         CSFS_CK(cudaEventRecord(c->w_copied, c->aux));
         const size_t nout = nt * size_t(ks.out_dim());
         c->h_out.grow(nout);
         csfmm_any(c, c->h_txyz.p, nt, dsrc, c->h_w.p, ns, ks, f, c->h_out.p, st, s, c->w_copied);
-        CSFS_CK(cudaMemcpyAsync(out, c->h_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
+        d2h_staged(c, out, c->h_out.p, nout * sizeof(double), s);
         CSFS_CK(cudaStreamSynchronize(s));
     });
 }

@@ -32,6 +32,10 @@ struct csfs_b200_ctx {
     csfs_b200::DevBuf<double> phi_near;
     csfs_b200::DevBuf<int> counter;
     csfs_b200::DevBuf<double> h_txyz, h_sxyz, h_w, h_out;  // staging for the host-pointer API
+    // pinned bounce buffers of the host-pointer API for PAGEABLE caller memory (capi.cu
+    // h2d_staged / d2h_staged): allocated on first use, two so a copy overlaps the DMA
+    void* stage_pin[2] = {nullptr, nullptr};
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};  // the last DMA that used each buffer
     csfs_b200::DevBuf<double> d_soa;
     csfs_b200::DevBuf<int4> d_items;
     csfs_b200::DevBuf<int2> d_segs;
