@@ -106,6 +106,10 @@ __global__ void __launch_bounds__(kCstcThreads)
 // back as broadcasts (the next chunk's loads in flight during the current chunk's
 // evaluation) instead of every lane issuing its own uniform-address loads and waiting on
 // them; the stack lives in shared memory instead of 1 KB of local memory per thread.
+#ifndef CSFS_CSTC_WARP_UNROLL
+#define CSFS_CSTC_WARP_UNROLL 8
+#endif
+constexpr int kCstcWarpUnroll = CSFS_CSTC_WARP_UNROLL;
 constexpr int kCstcWarpThreads = 512;  // 16 warps; 2 CTAs per SM (table 64 KB + 48 KB)
 constexpr int kCstcWarps = kCstcWarpThreads / 32;
 constexpr size_t kCstcWarpSmem =
@@ -169,13 +173,13 @@ __global__ void __launch_bounds__(kCstcWarpThreads, 2)
             }
             const int m = min(32, cnt - c0);
             if (act && guard) {
-#pragma unroll 4
+#pragma unroll kCstcWarpUnroll
                 for (int k = 0; k < m; ++k) {
                     const double2 a = sxy[k], b = szw[k];
                     op.template eval<true, false>(tx, ty, tz, a.x, a.y, b.x, b.y, acc, tab);
                 }
             } else if (act) {
-#pragma unroll 4
+#pragma unroll kCstcWarpUnroll
                 for (int k = 0; k < m; ++k) {
                     const double2 a = sxy[k], b = szw[k];
                     op.template eval<false, false>(tx, ty, tz, a.x, a.y, b.x, b.y, acc, tab);
