@@ -18,4 +18,13 @@ for c in c2 c3 c5; do TREE_MODES=sort timeout 300 python tools/tree_perf.py $c 5
 timeout 1200 python tools/bve_perf.py 9 > gpurun_out/bve_$T.log 2>&1
 timeout 1500 python tools/cstc_perf.py c2 c3 c5 > gpurun_out/cstc_$T.log 2>&1
 timeout 900 python tools/scaling_emulation.py c5 gpurun_out/scaling_${T}.json > gpurun_out/scaling_${T}.log 2>&1
+# the reference arm, the HBM-kernel ncu pass (every non-evaluation kernel) and the full-size parity run
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$T.json 2> gpurun_out/bench_ref_$T.err
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,launch__grid_size
+timeout 900 ncu --metrics $M --clock-control none -k "regex:^(?!k_interact|k_mutual|k_dfma).*" --csv --log-file gpurun_out/hbm_$T.csv python tools/prof_once.py c5 > gpurun_out/hbm_$T.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_fullsize.py -q -m gpu -s > gpurun_out/parity_fullsize_$T.log 2>&1
+rm -f gpurun_out/*.ncu-rep  # the raw-page CSVs are kept; the reports would pass gpurun's 64 MiB return limit
 echo done
+# then here: cp the outputs over profiles/r02_* (profiles/README.md lists them), python tools/launch_summary.py
+# gpurun_out/launches_$T.csv profiles/r02_launches_c5_step_summary.json, python tools/ncu_hbm_summary.py
+# gpurun_out/hbm_$T.csv profiles/r02_hbm_kernels_ncu.json
